@@ -1,0 +1,203 @@
+/*
+ * pinn_dd.h -- C ABI of the B200-native per-subdomain training step of parallel
+ * cPINN / XPINN (Shukla, Jagtap & Karniadakis, arXiv 2104.10013).
+ *
+ * Citation key: P:n = PAPER.md line n (LaTeX source of the paper).
+ *
+ * One handle owns the subdomains Omega_q placed on ONE GPU (one process per
+ * GPU).  For every owned subdomain it holds the network parameters Theta_q =
+ * {W^k, b^k, a^k}, the Adam state and borrowed pointers to
+ * the subdomain's point sets {x_F}, {x_u}, {x_I}.  The calls follow the
+ * red / green / optimisation stages of Algorithm 1:
+ *
+ *   pinn_dd_interface_payload  red, lines 238-243: u(x_I) and f(x_I).n (cPINN)
+ *                              or F(x_I) (XPINN) into the payload buffer
+ *   (exchange)                 green, lines 244-265: the caller moves payload
+ *                              rows of cut edges between ranks (torch.distributed
+ *                              / NCCL); intra-GPU neighbours need nothing
+ *   pinn_dd_loss_grad          line 253/261: J(Theta_q) of Eq. (5)/(6) and
+ *                              dJ/dTheta_q with neighbour values held constant
+ *   pinn_dd_adam               lines 266-267: one Adam step per subdomain
+ *   pinn_dd_step               all of the above for handles without remote
+ *                              neighbours, n_iters times, CUDA-graph replayed
+ *   pinn_dd_predict            Eq. (4) stitched solution
+ *
+ * Conventions
+ * -----------
+ * - All bulk arrays are DEVICE pointers, float32, caller-owned and BORROWED:
+ *   they must stay valid and unchanged until pinn_dd_destroy.  Host arrays in
+ *   the descriptor are deep-copied by pinn_dd_create.
+ * - Coordinates: x1 = x and x2 = t (Burgers, "time as one component of x")
+ *   or x2 = y (Poisson / heat / NS).  Arrays are SoA: coords[2][n_points].
+ * - Point order inside the handle: subdomain by subdomain; inside subdomain q
+ *   (points [sub_point_offset[q], sub_point_offset[q+1])): first the N_F
+ *   residual points, then the N_u training points, then the interface points
+ *   edge segment by edge segment (segments [sub_seg_offset[q],
+ *   sub_seg_offset[q+1]) of the seg_* arrays, seg_n[s] points each).
+ * - Parameters use the layer-major packing W^1, b^1, a^1, ..., W^{L-1},
+ *   b^{L-1}, a^{L-1}, W^L, b^L with W^k row-major N_k x N_{k-1} (the layout of
+ *   pinn_dd_n_params); internally the library pads each tensor to 16 bytes.
+ * - Every call returns a status and never throws or aborts across the ABI;
+ *   pinn_dd_last_error returns the message of the last failing call.
+ *   Asynchronous CUDA errors surface at the next call that synchronises.
+ * - Calls are stream-ordered on desc->stream.  Only calls with a HOST output
+ *   (pinn_dd_step with loss_host != NULL, pinn_dd_get_step) synchronise.
+ */
+#ifndef PINN_DD_H
+#define PINN_DD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pinn_dd pinn_dd; /* opaque, one per process (GPU) */
+
+typedef enum {
+  PINN_DD_OK = 0,
+  PINN_DD_EINVAL = 1,        /* shape / count / pointer mismatch, cPINN with a time-axis interface */
+  PINN_DD_EUNSUPPORTED = 2,  /* (width, n_hidden, d_out, activation) not compiled in */
+  PINN_DD_ECUDA = 3,         /* CUDA runtime error; message carries cudaGetErrorString */
+  PINN_DD_ENCCL = 4,         /* reserved */
+  PINN_DD_ENONFINITE = 5,    /* a loss J_q or gradient is NaN/Inf (message names the subdomain) */
+  PINN_DD_EPROTOCOL = 6      /* interface segment without a twin, remote twin used by pinn_dd_step */
+} pinn_dd_status;
+
+enum { PINN_DD_METHOD_PINN = 0, PINN_DD_METHOD_CPINN = 1, PINN_DD_METHOD_XPINN = 2 };
+/* P:313-316 Burgers; P:823-829 heat (K known; POISSON = K==1 with u* = sin(pi x) sin(pi y));
+   P:415-417 steady incompressible NS (outputs u, v, p). */
+enum { PINN_DD_PDE_BURGERS = 0, PINN_DD_PDE_POISSON = 1, PINN_DD_PDE_HEAT = 2, PINN_DD_PDE_NS = 3 };
+enum { PINN_DD_ACT_TANH = 0, PINN_DD_ACT_SIN = 1, PINN_DD_ACT_COS = 2 };
+
+/* flags */
+#define PINN_DD_FLAG_GRAPH        1  /* pinn_dd_step replays a captured CUDA graph */
+#define PINN_DD_FLAG_GLOBAL_STASH 2  /* keep the reverse-mode stash in global memory instead of TMEM (debug) */
+#define PINN_DD_FLAG_TIMING       4  /* record per-kernel CUDA events (see pinn_dd_kernel_times) */
+
+/* Per-subdomain hyper-parameters, P:151-161 (loss weights) and P:286 (Adam). */
+typedef struct {
+  float w_u;     /* W_u   data-mismatch weight                       */
+  float w_f;     /* W_F   residual weight                            */
+  float w_i;     /* W_I   average-solution interface weight          */
+  float w_if;    /* W_Iflux (cPINN) or W_IF (XPINN) interface weight */
+  float lr;      /* Adam learning rate                               */
+  float beta1, beta2, eps;
+} pinn_dd_hparams;
+
+typedef struct {
+  /* ---- problem ---------------------------------- */
+  int32_t method;      /* PINN_DD_METHOD_*                                   */
+  int32_t pde;         /* PINN_DD_PDE_*                                      */
+  int32_t activation;  /* PINN_DD_ACT_*                                      */
+  int32_t d_in;        /* must be 2                                          */
+  int32_t d_out;       /* 1, or 3 for NS                                     */
+  int32_t width;       /* N_k of every hidden layer                          */
+  int32_t n_hidden;    /* L-1 hidden layers                                  */
+  float slope_n;       /* n of the adaptive slope n a^k (n = 10)       */
+  float nu;            /* Burgers viscosity (0.01/pi)                 */
+  float re;            /* NS Reynolds number (100)                    */
+  /* ---- subdomains owned by this handle (host arrays, copied) ---------- */
+  int32_t n_sub;
+  const int32_t* sub_point_offset;  /* [n_sub+1]                              */
+  const int32_t* sub_n_res;         /* [n_sub]  N_F                           */
+  const int32_t* sub_n_data;        /* [n_sub]  N_u (may be 0)                */
+  const int32_t* sub_seg_offset;    /* [n_sub+1] into the seg_* arrays        */
+  const pinn_dd_hparams* sub_hparams; /* [n_sub]                              */
+  /* ---- interface edge segments (host arrays, copied) ------------------ */
+  int32_t n_seg;
+  const int32_t* seg_n;      /* [n_seg] N_I of the edge                             */
+  const float* seg_normal;   /* [n_seg][2] canonical unit normal of the edge */
+  const int64_t* seg_twin;   /* [n_seg] payload slot of the twin (neighbour's copy)
+                                of the segment's first point; slots < n_points are
+                                local points, slots >= n_points are received rows  */
+  /* ---- point table (DEVICE, borrowed) -------------------------------- */
+  int64_t n_points;
+  int64_t n_recv;            /* payload rows received from other ranks            */
+  const float* coords;       /* [2][n_points]                                      */
+  const float* target;       /* [d_out][n_points]   training targets u^(i)         */
+  const float* mask;         /* [d_out][n_points]   1 = constrained output         */
+  const float* init_params;  /* [n_sub][pinn_dd_n_params(...)] packed, or NULL = 0 */
+  /* ---- runtime --------------------------------------------------------- */
+  void* stream;              /* cudaStream_t (NULL = legacy default stream)        */
+  int32_t flags;             /* PINN_DD_FLAG_*                                     */
+} pinn_dd_desc;
+
+/* Number of packed parameters of one network [d_in, width x n_hidden, d_out]:
+   sum_k (N_k N_{k-1} + N_k) + (L-1) slopes. */
+int64_t pinn_dd_n_params(int32_t d_in, int32_t width, int32_t n_hidden, int32_t d_out);
+
+/* Device workspace the handle needs (bytes); the caller allocates it (e.g. a
+   torch uint8 tensor) and passes it to pinn_dd_create.  Alignment 256 B. */
+pinn_dd_status pinn_dd_workspace_size(const pinn_dd_desc* d, size_t* bytes);
+
+/* Validate the descriptor, plan tiles and chunks, copy the initial parameters
+   into the workspace (Adam m = v = 0, t = 0).  The workspace is borrowed. */
+pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* dev_workspace, size_t ws_bytes,
+                              pinn_dd** out);
+
+/* K2: u(x_I) and f(x_I).n (cPINN, Table 1) or F(x_I) (XPINN) of every
+   local interface point from the CURRENT parameters into the payload buffer
+   (Algorithm 1).  Row r of the buffer holds d_out + n_eq floats. */
+pinn_dd_status pinn_dd_interface_payload(pinn_dd* h);
+
+/* Payload buffer [n_points + n_recv][n_fields] (device, library-owned).  Rows
+   [0, n_points) are written by pinn_dd_interface_payload; rows [n_points,
+   n_points + n_recv) must be filled by the caller's exchange before
+   pinn_dd_loss_grad. n_fields = d_out + n_eq (n_eq = 3 for NS, else 1). */
+pinn_dd_status pinn_dd_payload_buffer(pinn_dd* h, float** buf, int32_t* n_fields, int64_t* n_rows);
+
+/* K1 + K5(reduce): J(Theta_q) (Eq. 5 cPINN / Eq. 6 XPINN / Eq. 3 if no live
+   interface) and g_q = dJ_q/dTheta_q with every neighbour value
+   constant, for all local q.  Requires a current payload buffer.
+   loss_dev (nullable): device [n_sub][8] = {MSE_u, MSE_F, MSE_uavg,
+   MSE_flux|MSE_R, J, 0, 0, 0}.  grad_dev (nullable): device [n_sub][n_params]
+   packed gradient. */
+pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev);
+
+/* K5(adam): one bias-corrected Adam step (beta1, beta2, eps, lr per subdomain)
+   on every local subdomain with the gradient of the last pinn_dd_loss_grad. */
+pinn_dd_status pinn_dd_adam(pinn_dd* h);
+
+/* n_iters x (payload -> loss+grad -> Adam), one synchronous Jacobi iteration
+   each (payloads from the parameters at the start of the iteration).  Only for
+   handles with n_recv == 0 (else PINN_DD_EPROTOCOL).  With PINN_DD_FLAG_GRAPH
+   the three launches are captured once and replayed.  loss_host (nullable):
+   host [n_sub][8] breakdown of the LAST iteration (synchronises); a non-finite
+   J returns PINN_DD_ENONFINITE. */
+pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host);
+
+/* K6: Eq. (4) stitched solution u(z) = sum_q u_q(z) 1_{Omega_q}(z) with weight
+   1/S at points shared by S subdomains.  pts: device [2][n]; owners: device
+   [n][4] local subdomain ids (-1 = unused), the caller's point classification;
+   out: device [d_out][n]. */
+pinn_dd_status pinn_dd_predict(pinn_dd* h, const float* pts, const int32_t* owners, int64_t n,
+                               float* out);
+
+/* Parameter / optimiser state access (device buffers of n_params floats,
+   packed layout).  what: 0 = Theta, 1 = Adam m, 2 = Adam v, 3 = last gradient. */
+pinn_dd_status pinn_dd_get_params(pinn_dd* h, int32_t sub, int32_t what, float* dst_dev);
+pinn_dd_status pinn_dd_set_params(pinn_dd* h, int32_t sub, int32_t what, const float* src_dev);
+/* Adam step counter t of subdomain `sub` (host; synchronises). */
+pinn_dd_status pinn_dd_get_step(pinn_dd* h, int32_t sub, int32_t* t);
+
+/* With PINN_DD_FLAG_TIMING: cumulative device milliseconds of
+   {K2 payload, K1 loss+grad, K5 reduce/adam, launches counted} since the last
+   call (synchronises, then resets). */
+pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4);
+
+/* Tile geometry chosen for this handle: {points per tile P, tiles per chunk,
+   number of chunks, grid size}. */
+pinn_dd_status pinn_dd_plan_info(pinn_dd* h, int64_t* info4);
+
+void pinn_dd_destroy(pinn_dd* h);
+
+/* Message of the last failing call on h (NULL h: the last pinn_dd_create /
+   workspace_size failure of this thread).  Never NULL. */
+const char* pinn_dd_last_error(const pinn_dd* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PINN_DD_H */

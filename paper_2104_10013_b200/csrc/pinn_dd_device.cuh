@@ -1,0 +1,345 @@
+// pinn_dd_device.cuh -- device-side building blocks of the fused sm_100a
+// cPINN / XPINN training step (arXiv 2104.10013).  P:n = PAPER.md line n.
+//
+// Forward-mode Taylor jets.  Every point carries C = 4 channels through the
+// network: value, d/dx1, d/dx2 and the masked Laplacian Delta_S (S = dims whose
+// pure second derivatives the operator needs; only pure seconds are needed,
+// never mixed ones).  For a hidden pre-activation z with jets (z, g1, g2, L)
+// and slope s = n a^k (reading Z6) the activation h = sigma(s z)
+// propagates as
+//   h_v = sigma(u),  h_i = sigma'(u) s g_i,  h_L = sigma''(u) s^2 Q + sigma'(u) s L,
+//   u = s z,  Q = sum_{i in S} g_i^2.
+// The reverse sweep (act_bwd) is the exact adjoint of that map, including the
+// derivative with respect to the slope s (for da^k = n dJ/ds).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pinn {
+
+constexpr int kThreads = 128;   // 4 warps = the 4 TMEM lane quarters
+constexpr int kC = 4;           // jet channels
+constexpr int kJT = 20;         // neurons per thread (mapping A)
+constexpr int kA = kC * kJT;    // stash floats per thread per hidden layer
+
+__host__ __device__ constexpr int al4(int x) { return (x + 3) & ~3; }
+
+// Internal (16-byte padded) parameter layout of one network
+// [2, N x NH, DO]; the packed layout of the ABI is W1 b1 a1 W2 b2 a2 ... WL bL.
+template <int N, int NH, int DO>
+struct Lay {
+  static constexpr int L = NH + 1;
+  __host__ __device__ static constexpr int nin(int k) { return k == 1 ? 2 : N; }
+  __host__ __device__ static constexpr int nout(int k) { return k == L ? DO : N; }
+  __host__ __device__ static constexpr int offW(int k) { return k == 1 ? 0 : al4(offA(k - 1) + 1); }
+  __host__ __device__ static constexpr int offB(int k) { return al4(offW(k) + nout(k) * nin(k)); }
+  __host__ __device__ static constexpr int offA(int k) { return al4(offB(k) + nout(k)); }
+  __host__ __device__ static constexpr int total() { return al4(offB(L) + DO); }
+};
+
+// Kernel geometry for width N (mapping A: thread = (point group pg, neuron block nb)).
+template <int N, int NH, int DO>
+struct KCfg {
+  static_assert(N % kJT == 0, "width must be a multiple of 20");
+  static constexpr int NB = N / kJT;           // neuron blocks
+  static constexpr int P = kThreads / NB;      // points per tile (1 point per thread)
+  static constexpr int PSTR = P + 1;           // float4 row stride of activation buffers (odd)
+  // W^k (k = 2..NH) rows: j*WS + (j/kJT)*4 floats (block skew against bank conflicts)
+  static constexpr int WS = al4(N);
+  static constexpr int WROWS = N * WS + NB * 4;            // floats per hidden W in smem
+  // mapping B (dW): JB x IB register block, interleaved rows, S point splits
+  static constexpr int JB = (N >= 80) ? 8 : 4;
+  static constexpr int IB = JB;
+  static constexpr int NJ = N / JB;
+  static constexpr int NI = N / IB;
+  static constexpr int NBLK = NJ * NI;
+  static constexpr int S = (kThreads / NBLK) >= 4 ? 4 : ((kThreads / NBLK) >= 2 ? 2 : 1);
+  // smem carve (in floats)
+  static constexpr int oW1 = 0;                            // [N][2]
+  static constexpr int oB1 = oW1 + 2 * N;                  // [N]
+  static constexpr int oWh = al4(oB1 + N);                 // NH-1 hidden layers
+  static constexpr int oBh = oWh + (NH - 1) * WROWS;       // [NH-1][N]
+  static constexpr int oWo = al4(oBh + (NH - 1) * N);      // [DO][WS]
+  static constexpr int oBo = oWo + DO * WS;                // [DO]
+  static constexpr int oSl = al4(oBo + DO);                // [NH] slopes s_k = n a^k
+  static constexpr int oBuf = al4(oSl + NH) ;              // 2 x [N][PSTR] float4
+  static constexpr int BUF = N * PSTR * 4;
+  static constexpr int oU = oBuf + 2 * BUF;                // [P][DO] float4
+  static constexpr int oX = oU + P * DO * 4;               // [2][P]
+  static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [32]
+  static constexpr int oDw = oRed + 32;                    // dW split scratch [S][NBLK][JB*IB] (S>1)
+  static constexpr int DWS = (S > 1) ? S * NBLK * JB * IB : 0;
+  static constexpr int TOTAL = al4(oDw + DWS + 4);         // + tmem address slot
+  static constexpr size_t SMEM = size_t(TOTAL) * 4;
+};
+
+// ----------------------------------------------------------------------------
+// activations sigma, sigma', sigma'', sigma''' (ACT: 0 tanh, 1 sin, 2 cos)
+// ----------------------------------------------------------------------------
+template <int ACT>
+__device__ __forceinline__ void act_derivs(float u, float& s0, float& s1, float& s2, float& s3) {
+  if (ACT == 0) {
+    float t = tanhf(u);
+    s0 = t;
+    s1 = 1.0f - t * t;
+    s2 = -2.0f * t * s1;
+    s3 = s1 * (6.0f * t * t - 2.0f);
+  } else if (ACT == 1) {
+    float sn, cs;
+    sincosf(u, &sn, &cs);
+    s0 = sn; s1 = cs; s2 = -sn; s3 = -cs;
+  } else {
+    float sn, cs;
+    sincosf(u, &sn, &cs);
+    s0 = cs; s1 = -sn; s2 = -cs; s3 = sn;
+  }
+}
+
+// forward jet map of one neuron: (z, g1, g2, L) -> (h_v, h_1, h_2, h_L)
+template <int ACT>
+__device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2) {
+  float s0, s1, s2, s3;
+  act_derivs<ACT>(s * z.x, s0, s1, s2, s3);
+  float Q = m1 * z.y * z.y + m2 * z.z * z.z;
+  float4 h;
+  h.x = s0;
+  h.y = s1 * s * z.y;
+  h.z = s1 * s * z.z;
+  h.w = s2 * s * s * Q + s1 * s * z.w;
+  return h;
+}
+
+// adjoint of act_fwd: given hb = dJ/dh (4 channels) and the stashed z-jets,
+// return zb = dJ/dz (4 channels) and accumulate dJ/ds into sbar.
+template <int ACT>
+__device__ __forceinline__ float4 act_bwd(float4 z, float4 hb, float s, float m1, float m2, float& sbar) {
+  float s0, s1, s2, s3;
+  act_derivs<ACT>(s * z.x, s0, s1, s2, s3);
+  float Q = m1 * z.y * z.y + m2 * z.z * z.z;
+  // primed adjoints (= adjoint / s); see DESIGN.md "activation adjoint"
+  float zb = hb.x * s1 + s * s2 * (hb.y * z.y + hb.z * z.z) + hb.w * (s3 * s * s * Q + s2 * s * z.w);
+  float g1 = hb.y * s1 + 2.0f * m1 * hb.w * s2 * s * z.y;
+  float g2 = hb.z * s1 + 2.0f * m2 * hb.w * s2 * s * z.z;
+  float lb = hb.w * s1;
+  sbar += zb * z.x + g1 * z.y + g2 * z.z + lb * z.w;
+  return make_float4(s * zb, s * g1, s * g2, s * lb);
+}
+
+// ----------------------------------------------------------------------------
+// TMEM stash: each thread keeps its own pre-activation jets of every hidden
+// layer in its TMEM lane (warp w owns lanes 32w..32w+31; 512 columns).
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(slot)));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+}
+__device__ __forceinline__ void tmem_dealloc512(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(taddr));
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};\n" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// load 16 columns and wait in the same asm block so the values are valid on exit
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Stash policy: TMEM (default) or a per-CTA global scratch (debug fallback).
+struct Stash {
+  uint32_t taddr;     // TMEM base of this thread's lane quarter
+  float* g;           // global fallback base for this CTA (or nullptr)
+  int tid;
+  __device__ __forceinline__ void store(int slot, const float* v) {
+    if (g == nullptr) {
+#pragma unroll
+      for (int q = 0; q < kA / 16; ++q) tmem_st16(taddr + slot * kA + q * 16, v + q * 16);
+      tmem_wait_st();
+    } else {
+#pragma unroll
+      for (int a = 0; a < kA; ++a) g[(size_t(slot) * kA + a) * kThreads + tid] = v[a];
+    }
+  }
+  __device__ __forceinline__ void load(int slot, float* v) {
+    if (g == nullptr) {
+#pragma unroll
+      for (int q = 0; q < kA / 16; ++q) tmem_ld16(taddr + slot * kA + q * 16, v + q * 16);
+    } else {
+#pragma unroll
+      for (int a = 0; a < kA; ++a) v[a] = g[(size_t(slot) * kA + a) * kThreads + tid];
+    }
+  }
+};
+
+// ----------------------------------------------------------------------------
+// pointwise operators.  U[o] = (u, d1 u, d2 u, Delta_S u) of output o.
+// r[e] and dr[e][o][c] = d r_e / d U[o].c
+// ----------------------------------------------------------------------------
+constexpr int PDE_BURGERS = 0, PDE_POISSON = 1, PDE_HEAT = 2, PDE_NS = 3;
+
+struct PdeConst {
+  int pde;
+  float nu, re;
+};
+
+__device__ __forceinline__ void heat_K(float x, float y, float& K, float& Kx, float& Ky) {
+  float e = __expf(0.1f * y);
+  float sn, cs;
+  sincosf(0.5f * x, &sn, &cs);
+  K = 20.0f + e * sn;
+  Kx = 0.5f * e * cs;
+  Ky = 0.1f * e * sn;
+}
+
+// residual F := L_x(u) - f
+template <int DO>
+__device__ __forceinline__ int pde_residual(const PdeConst& pc, const float4* U, float x, float y, float* r,
+                                            float (*dr)[DO][4]) {
+#pragma unroll
+  for (int e = 0; e < 3; ++e)
+#pragma unroll
+    for (int o = 0; o < DO; ++o) dr[e][o][0] = dr[e][o][1] = dr[e][o][2] = dr[e][o][3] = 0.0f;
+  if (pc.pde == PDE_BURGERS) {
+    // u_t + u u_x - nu u_xx; channels (u, u_x, u_t, u_xx)
+    const float4 u = U[0];
+    r[0] = u.z + u.x * u.y - pc.nu * u.w;
+    dr[0][0][0] = u.y; dr[0][0][1] = u.x; dr[0][0][2] = 1.0f; dr[0][0][3] = -pc.nu;
+    return 1;
+  } else if (pc.pde == PDE_POISSON) {
+    // Delta u - f, f = -2 pi^2 sin(pi x) sin(pi y) (reading Z15)
+    const float4 u = U[0];
+    const float PI = 3.14159265358979323846f;
+    float f = -2.0f * PI * PI * sinpif(x) * sinpif(y);
+    r[0] = u.w - f;
+    dr[0][0][3] = 1.0f;
+    return 1;
+  } else if (pc.pde == PDE_HEAT) {
+    // d_x(K u_x) + d_y(K u_y) - f, f = 4 exp(-0.1 y)
+    const float4 u = U[0];
+    float K, Kx, Ky;
+    heat_K(x, y, K, Kx, Ky);
+    float f = 4.0f * __expf(-0.1f * y);
+    r[0] = K * u.w + Kx * u.y + Ky * u.z - f;
+    dr[0][0][1] = Kx; dr[0][0][2] = Ky; dr[0][0][3] = K;
+    return 1;
+  } else {
+    // steady incompressible NS, outputs (u, v, p)
+    if constexpr (DO == 3) {
+      const float4 u = U[0], v = U[1], p = U[2];
+      const float ir = 1.0f / pc.re;
+      r[0] = u.x * u.y + v.x * u.z + p.y - u.w * ir;
+      r[1] = u.x * v.y + v.x * v.z + p.z - v.w * ir;
+      r[2] = u.y + v.z;
+      dr[0][0][0] = u.y; dr[0][0][1] = u.x; dr[0][0][2] = v.x; dr[0][0][3] = -ir;
+      dr[0][1][0] = u.z; dr[0][2][1] = 1.0f;
+      dr[1][0][0] = v.y; dr[1][1][0] = v.z; dr[1][1][1] = u.x; dr[1][1][2] = v.x; dr[1][1][3] = -ir;
+      dr[1][2][2] = 1.0f;
+      dr[2][0][1] = 1.0f; dr[2][1][2] = 1.0f;
+    }
+    return 3;
+  }
+}
+
+// normal flux f(u).n of the conservation form (cPINN; Table 1)
+template <int DO>
+__device__ __forceinline__ int pde_flux(const PdeConst& pc, const float4* U, float x, float y, float n1, float n2,
+                                        float* r, float (*dr)[DO][4]) {
+#pragma unroll
+  for (int e = 0; e < 3; ++e)
+#pragma unroll
+    for (int o = 0; o < DO; ++o) dr[e][o][0] = dr[e][o][1] = dr[e][o][2] = dr[e][o][3] = 0.0f;
+  if (pc.pde == PDE_BURGERS) {
+    // space-time flux (u^2/2 - nu u_x, u) . n (reading Z13)
+    const float4 u = U[0];
+    r[0] = (0.5f * u.x * u.x - pc.nu * u.y) * n1 + u.x * n2;
+    dr[0][0][0] = u.x * n1 + n2;
+    dr[0][0][1] = -pc.nu * n1;
+    return 1;
+  } else if (pc.pde == PDE_POISSON || pc.pde == PDE_HEAT) {
+    const float4 u = U[0];
+    float K = 1.0f, Kx, Ky;
+    if (pc.pde == PDE_HEAT) heat_K(x, y, K, Kx, Ky);
+    r[0] = K * (u.y * n1 + u.z * n2);
+    dr[0][0][1] = K * n1;
+    dr[0][0][2] = K * n2;
+    return 1;
+  } else {
+    if constexpr (DO == 3) {
+      const float4 u = U[0], v = U[1], p = U[2];
+      const float ir = 1.0f / pc.re;
+      r[0] = (u.x * u.x + p.x - u.y * ir) * n1 + (u.x * v.x - u.z * ir) * n2;
+      r[1] = (u.x * v.x - v.y * ir) * n1 + (v.x * v.x + p.x - v.z * ir) * n2;
+      r[2] = u.x * n1 + v.x * n2;
+      dr[0][0][0] = 2.0f * u.x * n1 + v.x * n2; dr[0][1][0] = u.x * n2; dr[0][2][0] = n1;
+      dr[0][0][1] = -ir * n1; dr[0][0][2] = -ir * n2;
+      dr[1][0][0] = v.x * n1; dr[1][1][0] = u.x * n1 + 2.0f * v.x * n2; dr[1][2][0] = n2;
+      dr[1][1][1] = -ir * n1; dr[1][1][2] = -ir * n2;
+      dr[2][0][0] = n1; dr[2][1][0] = n2;
+    }
+    return 3;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// kernel argument block
+// ----------------------------------------------------------------------------
+struct Chunk {
+  int32_t sub;     // local subdomain
+  int32_t start;   // first point
+  int32_t count;   // points (<= tiles_per_chunk * P)
+  int32_t pad;
+};
+
+struct KArgs {
+  const float* coords;      // [2][n_points]
+  const float* target;      // [DO][n_points]
+  const float* mask;        // [DO][n_points]
+  const int32_t* pinfo;     // kind (bits 0-1: 0 residual, 1 data, 2 interface) | seg << 2
+  const float* pinv;        // 1 / N of the point's class (per edge for interface points)
+  const int32_t* ptwin;     // payload row of the twin (interface points)
+  const float2* seg_normal; // [n_seg]
+  const float* params;      // internal [n_sub][PSTRIDE]
+  const float4* sub_w;      // [n_sub] (w_u, w_f, w_i, w_if)
+  const Chunk* chunks;
+  int n_chunks;
+  int64_t n_points;
+  int pstride;              // floats per subdomain in params / partial
+  float* partial;           // [n_chunks][pstride]
+  float* partial_loss;      // [n_chunks][4]
+  float* payload;           // [rows][NF]
+  float* gstash;            // global stash fallback (nullptr = TMEM)
+  PdeConst pc;
+  int method;               // 0 pinn, 1 cpinn, 2 xpinn
+  float slope_n;
+  float m1, m2;             // Laplacian mask (x1 in S, x2 in S)
+};
+
+}  // namespace pinn

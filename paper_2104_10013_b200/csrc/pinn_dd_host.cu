@@ -1,0 +1,739 @@
+// pinn_dd_host.cu -- host orchestration behind the C ABI of include/pinn_dd.h.
+//
+// Pre-processing stage of Algorithm 1 as it applies to one GPU:
+// validate the descriptor, classify every point (residual / training /
+// interface), derive 1/N per class and per edge (Eq. 5/6, reading Z2),
+// plan tiles and chunks, carve the workspace, and drive the kernels
+// K2 (payload) -> K1 (loss + grad) -> K5 (reduce + Adam) on the caller's stream,
+// optionally captured once into a CUDA graph.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pinn_dd.h"
+#include "pinn_dd_kernels.cuh"
+
+using namespace pinn;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+// -------------------------------------------------------------------------
+// compiled network shapes
+// -------------------------------------------------------------------------
+struct Ops {
+  int N, NH, DO, ACT;
+  int pstride;     // Lay::total()
+  int P;           // points per tile
+  size_t smem;     // dynamic smem of the fused kernel
+  void (*k1)(const KArgs&, int grid, size_t smem, cudaStream_t);
+  void (*k2)(const KArgs&, int grid, size_t smem, cudaStream_t);
+  void (*pred)(const float*, int, float, const float*, const int32_t*, int64_t, float*, cudaStream_t);
+  void (*packmap)(std::vector<int32_t>&);
+  cudaError_t (*setattr)(size_t);
+};
+
+template <int N, int NH, int DO, int ACT>
+struct Inst {
+  using C = KCfg<N, NH, DO>;
+  using LY = Lay<N, NH, DO>;
+  static size_t smem() { return std::max<size_t>(C::SMEM, 120 * 1024); }   // force 1 CTA / SM (TMEM owner)
+  static void k1(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_fused<N, NH, DO, ACT, 0><<<grid, kThreads, sm, s>>>(a);
+  }
+  static void k2(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_fused<N, NH, DO, ACT, 1><<<grid, kThreads, sm, s>>>(a);
+  }
+  static void pred(const float* params, int pstride, float sn, const float* pts, const int32_t* own, int64_t n,
+                   float* out, cudaStream_t s) {
+    const int bs = 128;
+    const int64_t g = (n + bs - 1) / bs;
+    if (g > 0) k_predict<N, NH, DO, ACT><<<unsigned(g), bs, 0, s>>>(params, pstride, sn, pts, own, n, out);
+  }
+  // packed index -> internal offset (layer-major W, b, a)
+  static void packmap(std::vector<int32_t>& m) {
+    m.clear();
+    for (int k = 1; k <= NH + 1; ++k) {
+      const int nw = LY::nout(k) * LY::nin(k);
+      for (int e = 0; e < nw; ++e) m.push_back(LY::offW(k) + e);
+      for (int e = 0; e < LY::nout(k); ++e) m.push_back(LY::offB(k) + e);
+      if (k <= NH) m.push_back(LY::offA(k));
+    }
+  }
+  static cudaError_t setattr(size_t sm) {
+    cudaError_t e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sm));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  }
+  static Ops ops() {
+    return Ops{N, NH, DO, ACT, LY::total(), C::P, smem(), &k1, &k2, &pred, &packmap, &setattr};
+  }
+};
+
+// The shapes of BASELINE.json configs C1-C4 (tanh): 3x20, 5x20, 6x40, 5x80 (D_o = 3).
+const Ops* find_ops(int N, int NH, int DO, int ACT) {
+  static const Ops table[] = {
+      Inst<20, 3, 1, 0>::ops(), Inst<20, 5, 1, 0>::ops(), Inst<40, 6, 1, 0>::ops(), Inst<80, 5, 3, 0>::ops(),
+  };
+  for (const Ops& o : table)
+    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT) return &o;
+  return nullptr;
+}
+
+}  // namespace
+
+struct pinn_dd {
+  // copied descriptor + owned host arrays
+  pinn_dd_desc d;
+  std::vector<int32_t> sub_off, n_res, n_data, seg_off, seg_n;
+  std::vector<int64_t> seg_twin;
+  std::vector<float> seg_normal;
+  std::vector<pinn_dd_hparams> hp;
+  const Ops* ops = nullptr;
+  int nf = 0, neq = 0, n_packed = 0, pstride = 0;
+  int nsm = 148;
+  // plan
+  int n_chunks1 = 0, n_chunks2 = 0, grid1 = 0, grid2 = 0, tpc = 1;
+  // device (carved from the workspace)
+  float *params = nullptr, *m = nullptr, *v = nullptr, *grad = nullptr;
+  float *partial = nullptr, *partial_loss = nullptr, *payload = nullptr, *loss = nullptr;
+  float *pinv = nullptr, *gstash = nullptr, *scratch = nullptr;
+  int32_t *pinfo = nullptr, *ptwin = nullptr, *sub_chunk = nullptr, *tstep = nullptr, *done = nullptr;
+  int32_t *flag = nullptr, *packmap = nullptr;
+  float2* segn = nullptr;
+  float4 *sub_w = nullptr, *sub_adam = nullptr;
+  Chunk *chunks1 = nullptr, *chunks2 = nullptr;
+  cudaStream_t stream = nullptr;
+  // graph
+  cudaGraphExec_t gexec = nullptr;
+  // timing
+  cudaEvent_t ev[6] = {};
+  double ms[3] = {0, 0, 0};
+  long long launches = 0;
+  std::string err;
+};
+
+namespace {
+
+pinn_dd_status fail(pinn_dd* h, pinn_dd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h)
+    h->err = buf;
+  else
+    g_create_error = buf;
+  return s;
+}
+
+#define CK(h, call)                                                                                         \
+  do {                                                                                                      \
+    cudaError_t e_ = (call);                                                                                \
+    if (e_ != cudaSuccess) return fail(h, PINN_DD_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                                  \
+  } while (0)
+
+int n_eq_of(int pde) { return pde == PINN_DD_PDE_NS ? 3 : 1; }
+
+// tiles per chunk of a subdomain with `cnt` points: >= 4 tiles, <= ~128 chunks
+int chunk_tiles(int cnt, int P) {
+  const int tiles = (cnt + P - 1) / P;
+  return std::max(4, (tiles + 127) / 128);
+}
+
+struct Carve {
+  size_t off = 0;
+  template <class T>
+  size_t take(size_t count) {
+    size_t o = off;
+    off += (count * sizeof(T) + 255) & ~size_t(255);
+    return o;
+  }
+};
+
+struct Layout {
+  size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, ch1, ch2, subch,
+      tstep, done, flag, loss, packmap, gstash, total;
+};
+
+// validation + planning shared by workspace_size and create
+pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
+  if (!d) return fail(h, PINN_DD_EINVAL, "desc is NULL");
+  if (d->d_in != 2) return fail(h, PINN_DD_EINVAL, "d_in must be 2 (got %d)", d->d_in);
+  if (d->method < 0 || d->method > 2) return fail(h, PINN_DD_EINVAL, "bad method %d", d->method);
+  if (d->pde < 0 || d->pde > 3) return fail(h, PINN_DD_EINVAL, "bad pde %d", d->pde);
+  const int want_do = d->pde == PINN_DD_PDE_NS ? 3 : 1;
+  if (d->d_out != want_do) return fail(h, PINN_DD_EINVAL, "d_out %d does not match pde %d", d->d_out, d->pde);
+  const Ops* ops = find_ops(d->width, d->n_hidden, d->d_out, d->activation);
+  if (!ops)
+    return fail(h, PINN_DD_EUNSUPPORTED, "network [2, %dx%d, %d] activation %d not compiled in", d->width,
+                d->n_hidden, d->d_out, d->activation);
+  if (d->n_sub < 1) return fail(h, PINN_DD_EINVAL, "n_sub must be >= 1");
+  if (!d->sub_point_offset || !d->sub_n_res || !d->sub_n_data || !d->sub_seg_offset || !d->sub_hparams)
+    return fail(h, PINN_DD_EINVAL, "subdomain arrays must not be NULL");
+  if (d->n_seg > 0 && (!d->seg_n || !d->seg_normal || !d->seg_twin))
+    return fail(h, PINN_DD_EINVAL, "segment arrays must not be NULL");
+  if (d->method == PINN_DD_METHOD_PINN && d->n_seg != 0)
+    return fail(h, PINN_DD_EINVAL, "method PINN has no interfaces");
+  if (d->n_points < 0 || d->n_recv < 0) return fail(h, PINN_DD_EINVAL, "negative counts");
+  if (d->n_points > 0 && !d->coords) return fail(h, PINN_DD_EINVAL, "coords is NULL");
+  if (d->n_points >= (int64_t(1) << 31) || d->n_points + d->n_recv >= (int64_t(1) << 31))
+    return fail(h, PINN_DD_EINVAL, "too many points for int32 indexing");
+  if (d->sub_point_offset[0] != 0 || d->sub_seg_offset[0] != 0)
+    return fail(h, PINN_DD_EINVAL, "offsets must start at 0");
+  if (d->sub_point_offset[d->n_sub] != d->n_points)
+    return fail(h, PINN_DD_EINVAL, "sub_point_offset[n_sub] != n_points");
+  if (d->sub_seg_offset[d->n_sub] != d->n_seg) return fail(h, PINN_DD_EINVAL, "sub_seg_offset[n_sub] != n_seg");
+  bool any_data = false;
+  for (int q = 0; q < d->n_sub; ++q) {
+    const int64_t cnt = int64_t(d->sub_point_offset[q + 1]) - d->sub_point_offset[q];
+    if (cnt < 0 || d->sub_n_res[q] < 0 || d->sub_n_data[q] < 0)
+      return fail(h, PINN_DD_EINVAL, "subdomain %d: negative count", q);
+    if (d->sub_seg_offset[q + 1] < d->sub_seg_offset[q])
+      return fail(h, PINN_DD_EINVAL, "subdomain %d: seg offsets not monotone", q);
+    int64_t ni = 0;
+    for (int s = d->sub_seg_offset[q]; s < d->sub_seg_offset[q + 1]; ++s) {
+      if (d->seg_n[s] < 1) return fail(h, PINN_DD_EINVAL, "segment %d: N_I must be >= 1", s);
+      ni += d->seg_n[s];
+    }
+    if (d->sub_n_res[q] + d->sub_n_data[q] + ni != cnt)
+      return fail(h, PINN_DD_EINVAL, "subdomain %d: N_F + N_u + sum N_I = %lld != %lld points", q,
+                  (long long)(d->sub_n_res[q] + d->sub_n_data[q] + ni), (long long)cnt);
+    if (d->sub_n_data[q] > 0) any_data = true;
+  }
+  if (any_data && (!d->target || !d->mask)) return fail(h, PINN_DD_EINVAL, "target/mask NULL with training points");
+  for (int s = 0; s < d->n_seg; ++s) {
+    const float n1 = d->seg_normal[2 * s], n2 = d->seg_normal[2 * s + 1];
+    if (std::fabs(n1 * n1 + n2 * n2 - 1.0f) > 1e-5f) return fail(h, PINN_DD_EINVAL, "segment %d: normal not unit", s);
+    if (d->method == PINN_DD_METHOD_CPINN && d->pde == PINN_DD_PDE_BURGERS && n2 != 0.0f)
+      return fail(h, PINN_DD_EINVAL,
+                  "cPINN with a time-axis interface (segment %d) is not allowed (P:816, SPEC.md:689)", s);
+    const int64_t tw = d->seg_twin[s];
+    if (tw < 0 || tw + d->seg_n[s] > d->n_points + d->n_recv)
+      return fail(h, PINN_DD_EPROTOCOL, "segment %d: twin rows [%lld, +%d) out of range", s, (long long)tw,
+                  d->seg_n[s]);
+  }
+  // tiles and chunks.  The chunking of a subdomain depends only on its own
+  // point count (never on which other subdomains share the GPU), so the
+  // fixed-order reduction is bitwise placement-invariant.
+  const int P = ops->P;
+  int n1 = 0, n2 = 0;
+  for (int q = 0; q < d->n_sub; ++q) {
+    const int cnt = d->sub_point_offset[q + 1] - d->sub_point_offset[q];
+    const int span = chunk_tiles(cnt, P) * P;
+    n1 += std::max(1, (cnt + span - 1) / span);
+    const int ni = cnt - d->sub_n_res[q] - d->sub_n_data[q];
+    n2 += (ni + P - 1) / P;
+  }
+  const int pstride = ops->pstride;
+  const int nf = d->d_out + n_eq_of(d->pde);
+  const size_t ns = size_t(d->n_sub);
+  const size_t npt = size_t(d->n_points);
+  const int grid1 = std::min(n1, nsm);
+  Carve c;
+  L->params = c.take<float>(ns * pstride);
+  L->m = c.take<float>(ns * pstride);
+  L->v = c.take<float>(ns * pstride);
+  L->grad = c.take<float>(ns * pstride);
+  L->scratch = c.take<float>(ns * pstride);
+  L->partial = c.take<float>(size_t(n1) * pstride);
+  L->ploss = c.take<float>(size_t(n1) * 4);
+  L->payload = c.take<float>((npt + size_t(d->n_recv) + 1) * nf);
+  L->pinfo = c.take<int32_t>(npt + 1);
+  L->pinv = c.take<float>(npt + 1);
+  L->ptwin = c.take<int32_t>(npt + 1);
+  L->segn = c.take<float2>(size_t(d->n_seg) + 1);
+  L->subw = c.take<float4>(ns);
+  L->suba = c.take<float4>(ns);
+  L->ch1 = c.take<Chunk>(size_t(n1));
+  L->ch2 = c.take<Chunk>(size_t(n2) + 1);
+  L->subch = c.take<int32_t>(ns + 1);
+  L->tstep = c.take<int32_t>(ns);
+  L->done = c.take<int32_t>(ns);
+  L->flag = c.take<int32_t>(1);
+  L->loss = c.take<float>(ns * 8);
+  L->packmap = c.take<int32_t>(size_t(pstride));
+  L->gstash = (d->flags & PINN_DD_FLAG_GLOBAL_STASH)
+                  ? c.take<float>(size_t(grid1) * d->n_hidden * kA * kThreads)
+                  : c.off;
+  L->total = c.off;
+  if (h) {
+    h->ops = ops;
+    h->tpc = chunk_tiles(d->n_sub ? d->sub_point_offset[1] - d->sub_point_offset[0] : 0, P);
+    h->n_chunks1 = n1;
+    h->n_chunks2 = n2;
+    h->grid1 = grid1;
+    h->grid2 = std::max(1, std::min(n2, nsm));
+    h->pstride = pstride;
+    h->nf = nf;
+    h->neq = n_eq_of(d->pde);
+  }
+  return PINN_DD_OK;
+}
+
+int device_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
+  KArgs a;
+  const pinn_dd_desc& d = h->d;
+  a.coords = d.coords;
+  a.target = d.target;
+  a.mask = d.mask;
+  a.pinfo = h->pinfo;
+  a.pinv = h->pinv;
+  a.ptwin = h->ptwin;
+  a.seg_normal = h->segn;
+  a.params = h->params;
+  a.sub_w = h->sub_w;
+  a.chunks = payload_tiles ? h->chunks2 : h->chunks1;
+  a.n_chunks = payload_tiles ? h->n_chunks2 : h->n_chunks1;
+  a.n_points = d.n_points;
+  a.pstride = h->pstride;
+  a.partial = h->partial;
+  a.partial_loss = h->partial_loss;
+  a.payload = h->payload;
+  a.gstash = (d.flags & PINN_DD_FLAG_GLOBAL_STASH) ? h->gstash : nullptr;
+  a.pc.pde = d.pde;
+  a.pc.nu = d.nu;
+  a.pc.re = d.re;
+  a.method = d.method;
+  a.slope_n = d.slope_n;
+  // S of Delta_S: Burgers needs u_xx only (x1); the 2-D operators need both
+  a.m1 = 1.0f;
+  a.m2 = d.pde == PINN_DD_PDE_BURGERS ? 0.0f : 1.0f;
+  return a;
+}
+
+RArgs make_rargs(pinn_dd* h, int mode) {
+  RArgs r;
+  r.partial = h->partial;
+  r.partial_loss = h->partial_loss;
+  r.sub_chunk = h->sub_chunk;
+  r.pstride = h->pstride;
+  r.grad = h->grad;
+  r.params = h->params;
+  r.m = h->m;
+  r.v = h->v;
+  r.tstep = h->tstep;
+  r.done = h->done;
+  r.sub_w = h->sub_w;
+  r.sub_adam = h->sub_adam;
+  r.loss = h->loss;
+  r.flag = h->flag;
+  r.mode = mode;
+  return r;
+}
+
+const int kRB = 256;
+
+pinn_dd_status launch_k2(pinn_dd* h) {
+  if (h->n_chunks2 == 0) return PINN_DD_OK;
+  h->ops->k2(make_kargs(h, true), h->grid2, h->ops->smem, h->stream);
+  ++h->launches;
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+pinn_dd_status launch_k1(pinn_dd* h) {
+  h->ops->k1(make_kargs(h, false), h->grid1, h->ops->smem, h->stream);
+  ++h->launches;
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+pinn_dd_status launch_k5(pinn_dd* h, int mode) {
+  dim3 g((h->pstride + kRB - 1) / kRB, h->d.n_sub);
+  k_reduce_adam<<<g, kRB, 0, h->stream>>>(make_rargs(h, mode));
+  ++h->launches;
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+
+pinn_dd_status one_iteration(pinn_dd* h, bool timed) {
+  pinn_dd_status s;
+  if (timed) CK(h, cudaEventRecord(h->ev[0], h->stream));
+  if ((s = launch_k2(h)) != PINN_DD_OK) return s;
+  if (timed) CK(h, cudaEventRecord(h->ev[1], h->stream));
+  if ((s = launch_k1(h)) != PINN_DD_OK) return s;
+  if (timed) CK(h, cudaEventRecord(h->ev[2], h->stream));
+  if ((s = launch_k5(h, 1)) != PINN_DD_OK) return s;
+  if (timed) {
+    CK(h, cudaEventRecord(h->ev[3], h->stream));
+    CK(h, cudaEventSynchronize(h->ev[3]));
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, h->ev[0], h->ev[1]);
+    cudaEventElapsedTime(&b, h->ev[1], h->ev[2]);
+    cudaEventElapsedTime(&c, h->ev[2], h->ev[3]);
+    h->ms[0] += a;
+    h->ms[1] += b;
+    h->ms[2] += c;
+  }
+  return PINN_DD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t pinn_dd_n_params(int32_t d_in, int32_t width, int32_t n_hidden, int32_t d_out) {
+  if (d_in < 1 || width < 1 || n_hidden < 1 || d_out < 1) return -1;
+  int64_t n = int64_t(width) * d_in + width + 1;
+  n += int64_t(n_hidden - 1) * (int64_t(width) * width + width + 1);
+  n += int64_t(d_out) * width + d_out;
+  return n;
+}
+
+pinn_dd_status pinn_dd_workspace_size(const pinn_dd_desc* d, size_t* bytes) {
+  if (!bytes) return fail(nullptr, PINN_DD_EINVAL, "bytes is NULL");
+  Layout L;
+  pinn_dd_status s = plan(d, nullptr, &L, device_sms());
+  if (s != PINN_DD_OK) return s;
+  *bytes = L.total;
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, pinn_dd** out) {
+  if (!out) return fail(nullptr, PINN_DD_EINVAL, "out is NULL");
+  *out = nullptr;
+  pinn_dd* h = new pinn_dd();
+  Layout L;
+  h->nsm = device_sms();
+  pinn_dd_status s = plan(d, h, &L, h->nsm);
+  if (s != PINN_DD_OK) {
+    g_create_error = h->err;
+    delete h;
+    return s;
+  }
+  if (!ws || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(ws) & 255u)) {
+    fail(nullptr, PINN_DD_EINVAL, "workspace %p of %zu bytes; need %zu bytes, 256-B aligned", ws, ws_bytes, L.total);
+    delete h;
+    return PINN_DD_EINVAL;
+  }
+  // deep copies of the host arrays
+  h->d = *d;
+  const int ns = d->n_sub;
+  h->sub_off.assign(d->sub_point_offset, d->sub_point_offset + ns + 1);
+  h->n_res.assign(d->sub_n_res, d->sub_n_res + ns);
+  h->n_data.assign(d->sub_n_data, d->sub_n_data + ns);
+  h->seg_off.assign(d->sub_seg_offset, d->sub_seg_offset + ns + 1);
+  h->hp.assign(d->sub_hparams, d->sub_hparams + ns);
+  if (d->n_seg > 0) {
+    h->seg_n.assign(d->seg_n, d->seg_n + d->n_seg);
+    h->seg_twin.assign(d->seg_twin, d->seg_twin + d->n_seg);
+    h->seg_normal.assign(d->seg_normal, d->seg_normal + 2 * d->n_seg);
+  }
+  h->d.sub_point_offset = h->sub_off.data();
+  h->d.sub_n_res = h->n_res.data();
+  h->d.sub_n_data = h->n_data.data();
+  h->d.sub_seg_offset = h->seg_off.data();
+  h->d.sub_hparams = h->hp.data();
+  h->d.seg_n = h->seg_n.data();
+  h->d.seg_twin = h->seg_twin.data();
+  h->d.seg_normal = h->seg_normal.data();
+  h->stream = static_cast<cudaStream_t>(d->stream);
+
+  char* base = static_cast<char*>(ws);
+  h->params = reinterpret_cast<float*>(base + L.params);
+  h->m = reinterpret_cast<float*>(base + L.m);
+  h->v = reinterpret_cast<float*>(base + L.v);
+  h->grad = reinterpret_cast<float*>(base + L.grad);
+  h->scratch = reinterpret_cast<float*>(base + L.scratch);
+  h->partial = reinterpret_cast<float*>(base + L.partial);
+  h->partial_loss = reinterpret_cast<float*>(base + L.ploss);
+  h->payload = reinterpret_cast<float*>(base + L.payload);
+  h->pinfo = reinterpret_cast<int32_t*>(base + L.pinfo);
+  h->pinv = reinterpret_cast<float*>(base + L.pinv);
+  h->ptwin = reinterpret_cast<int32_t*>(base + L.ptwin);
+  h->segn = reinterpret_cast<float2*>(base + L.segn);
+  h->sub_w = reinterpret_cast<float4*>(base + L.subw);
+  h->sub_adam = reinterpret_cast<float4*>(base + L.suba);
+  h->chunks1 = reinterpret_cast<Chunk*>(base + L.ch1);
+  h->chunks2 = reinterpret_cast<Chunk*>(base + L.ch2);
+  h->sub_chunk = reinterpret_cast<int32_t*>(base + L.subch);
+  h->tstep = reinterpret_cast<int32_t*>(base + L.tstep);
+  h->done = reinterpret_cast<int32_t*>(base + L.done);
+  h->flag = reinterpret_cast<int32_t*>(base + L.flag);
+  h->loss = reinterpret_cast<float*>(base + L.loss);
+  h->packmap = reinterpret_cast<int32_t*>(base + L.packmap);
+  h->gstash = reinterpret_cast<float*>(base + L.gstash);
+
+  // ---- per-point classification and 1/N (Eq. 3/5/6; per-edge mean, Z2)
+  const int64_t np = d->n_points;
+  std::vector<int32_t> pinfo(np + 1, 0), ptwin(np + 1, 0);
+  std::vector<float> pinv(np + 1, 0.0f);
+  for (int q = 0; q < ns; ++q) {
+    const int64_t off = h->sub_off[q];
+    const int nr = h->n_res[q], nd = h->n_data[q];
+    for (int64_t p = off; p < off + nr; ++p) {
+      pinfo[p] = 0;
+      pinv[p] = 1.0f / float(nr);
+    }
+    for (int64_t p = off + nr; p < off + nr + nd; ++p) {
+      pinfo[p] = 1;
+      pinv[p] = 1.0f / float(nd);
+    }
+    int64_t p = off + nr + nd;
+    for (int sgi = h->seg_off[q]; sgi < h->seg_off[q + 1]; ++sgi) {
+      const int n = h->seg_n[sgi];
+      for (int j = 0; j < n; ++j, ++p) {
+        pinfo[p] = 2 | (sgi << 2);
+        pinv[p] = 1.0f / float(n);
+        ptwin[p] = int32_t(h->seg_twin[sgi] + j);
+      }
+    }
+  }
+  // a local twin must itself be an interface point
+  for (int sgi = 0; sgi < d->n_seg; ++sgi) {
+    const int64_t tw = h->seg_twin[sgi];
+    if (tw < np) {
+      for (int j = 0; j < h->seg_n[sgi]; ++j)
+        if ((pinfo[tw + j] & 3) != 2) {
+          s = fail(nullptr, PINN_DD_EPROTOCOL, "segment %d: twin row %lld is not an interface point", sgi,
+                   (long long)(tw + j));
+          delete h;
+          return s;
+        }
+    }
+  }
+  std::vector<float4> subw(ns), suba(ns);
+  for (int q = 0; q < ns; ++q) {
+    subw[q] = make_float4(h->hp[q].w_u, h->hp[q].w_f, h->hp[q].w_i, h->hp[q].w_if);
+    suba[q] = make_float4(h->hp[q].lr, h->hp[q].beta1, h->hp[q].beta2, h->hp[q].eps);
+  }
+  // ---- chunks: K1 over all points, K2 over interface points
+  const int P = h->ops->P;
+  std::vector<Chunk> c1, c2;
+  std::vector<int32_t> subch(ns + 1, 0);
+  for (int q = 0; q < ns; ++q) {
+    subch[q] = int32_t(c1.size());
+    const int off = h->sub_off[q], cnt = h->sub_off[q + 1] - off;
+    const int span = chunk_tiles(cnt, P) * P;
+    if (cnt == 0) c1.push_back(Chunk{q, off, 0, 0});
+    for (int s0 = 0; s0 < cnt; s0 += span) c1.push_back(Chunk{q, off + s0, std::min(span, cnt - s0), 0});
+    const int i0 = off + h->n_res[q] + h->n_data[q];
+    const int ni = h->sub_off[q + 1] - i0;
+    for (int s0 = 0; s0 < ni; s0 += P) c2.push_back(Chunk{q, i0 + s0, std::min(P, ni - s0), 0});
+  }
+  subch[ns] = int32_t(c1.size());
+  std::vector<int32_t> pm;
+  h->ops->packmap(pm);
+  h->n_packed = int(pm.size());
+
+  cudaStream_t st = h->stream;
+#define CKC(call)                                                                                  \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      fail(nullptr, PINN_DD_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));                       \
+      delete h;                                                                                    \
+      return PINN_DD_ECUDA;                                                                        \
+    }                                                                                              \
+  } while (0)
+  CKC(h->ops->setattr(h->ops->smem));
+  const size_t pbytes = size_t(ns) * h->pstride * sizeof(float);
+  CKC(cudaMemsetAsync(h->params, 0, pbytes, st));
+  CKC(cudaMemsetAsync(h->m, 0, pbytes, st));
+  CKC(cudaMemsetAsync(h->v, 0, pbytes, st));
+  CKC(cudaMemsetAsync(h->grad, 0, pbytes, st));
+  CKC(cudaMemsetAsync(h->payload, 0, (size_t(np) + d->n_recv + 1) * h->nf * sizeof(float), st));
+  CKC(cudaMemcpyAsync(h->pinfo, pinfo.data(), pinfo.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->pinv, pinv.data(), pinv.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->ptwin, ptwin.data(), ptwin.size() * 4, cudaMemcpyHostToDevice, st));
+  if (d->n_seg > 0)
+    CKC(cudaMemcpyAsync(h->segn, h->seg_normal.data(), h->seg_normal.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->sub_w, subw.data(), subw.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->sub_adam, suba.data(), suba.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->chunks1, c1.data(), c1.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
+  if (!c2.empty())
+    CKC(cudaMemcpyAsync(h->chunks2, c2.data(), c2.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->sub_chunk, subch.data(), subch.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemsetAsync(h->tstep, 0, ns * 4, st));
+  CKC(cudaMemsetAsync(h->done, 0, ns * 4, st));
+  CKC(cudaMemsetAsync(h->flag, 0, 4, st));
+  CKC(cudaMemsetAsync(h->loss, 0, ns * 8 * 4, st));
+  CKC(cudaMemcpyAsync(h->packmap, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice, st));
+  if (d->init_params) {
+    dim3 g((h->n_packed + 255) / 256, ns);
+    k_scatter<<<g, 256, 0, st>>>(d->init_params, h->packmap, h->n_packed, h->pstride, h->n_packed, h->params, ns);
+    CKC(cudaGetLastError());
+  }
+  for (auto& e : h->ev) CKC(cudaEventCreate(&e));
+  CKC(cudaStreamSynchronize(st));   // host vectors above go out of scope
+  *out = h;
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_interface_payload(pinn_dd* h) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  return launch_k2(h);
+}
+
+pinn_dd_status pinn_dd_payload_buffer(pinn_dd* h, float** buf, int32_t* n_fields, int64_t* n_rows) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  if (buf) *buf = h->payload;
+  if (n_fields) *n_fields = h->nf;
+  if (n_rows) *n_rows = h->d.n_points + h->d.n_recv;
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  pinn_dd_status s;
+  if ((s = launch_k1(h)) != PINN_DD_OK) return s;
+  if ((s = launch_k5(h, 0)) != PINN_DD_OK) return s;
+  if (loss_dev)
+    CK(h, cudaMemcpyAsync(loss_dev, h->loss, size_t(h->d.n_sub) * 8 * 4, cudaMemcpyDeviceToDevice, h->stream));
+  if (grad_dev) {
+    dim3 g((h->n_packed + 255) / 256, h->d.n_sub);
+    k_gather<<<g, 256, 0, h->stream>>>(h->grad, h->packmap, h->n_packed, h->pstride, h->n_packed, grad_dev,
+                                       h->d.n_sub);
+    CK(h, cudaGetLastError());
+  }
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_adam(pinn_dd* h) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  return launch_k5(h, 2);
+}
+
+pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  if (h->d.n_recv > 0)
+    return fail(h, PINN_DD_EPROTOCOL, "pinn_dd_step needs all twins local (n_recv = %lld); use the phased calls",
+                (long long)h->d.n_recv);
+  if (n_iters < 0) return fail(h, PINN_DD_EINVAL, "n_iters < 0");
+  const bool timed = (h->d.flags & PINN_DD_FLAG_TIMING) != 0;
+  const bool graph = (h->d.flags & PINN_DD_FLAG_GRAPH) != 0 && !timed;
+  pinn_dd_status s;
+  for (int it = 0; it < n_iters; ++it) {
+    if (graph) {
+      if (!h->gexec) {
+        cudaGraph_t g;
+        const long long before = h->launches;
+        CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        pinn_dd_status cs = one_iteration(h, false);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+        if (cs != PINN_DD_OK) return cs;
+        if (e != cudaSuccess) return fail(h, PINN_DD_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        CK(h, cudaGraphInstantiate(&h->gexec, g, 0));
+        cudaGraphDestroy(g);
+        h->launches = before;   // counted on every replay below
+      }
+      CK(h, cudaGraphLaunch(h->gexec, h->stream));
+      h->launches += (h->n_chunks2 > 0 ? 3 : 2);
+    } else if ((s = one_iteration(h, timed)) != PINN_DD_OK) {
+      return s;
+    }
+  }
+  if (loss_host) {
+    CK(h, cudaMemcpyAsync(loss_host, h->loss, size_t(h->d.n_sub) * 8 * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    int flag = 0;
+    CK(h, cudaMemcpy(&flag, h->flag, 4, cudaMemcpyDeviceToHost));
+    if (flag) {
+      CK(h, cudaMemset(h->flag, 0, 4));
+      for (int q = 0; q < h->d.n_sub; ++q)
+        if (!(loss_host[q * 8 + 4] == loss_host[q * 8 + 4]) || loss_host[q * 8 + 5] != 0.0f)
+          return fail(h, PINN_DD_ENONFINITE, "non-finite J in subdomain %d", q);
+      return fail(h, PINN_DD_ENONFINITE, "non-finite gradient (flag %d)", flag);
+    }
+  }
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_predict(pinn_dd* h, const float* pts, const int32_t* owners, int64_t n, float* out) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  if (n < 0 || (n > 0 && (!pts || !owners || !out))) return fail(h, PINN_DD_EINVAL, "bad predict arguments");
+  h->ops->pred(h->params, h->pstride, h->d.slope_n, pts, owners, n, out, h->stream);
+  ++h->launches;
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+
+static float* state_ptr(pinn_dd* h, int what) {
+  switch (what) {
+    case 0: return h->params;
+    case 1: return h->m;
+    case 2: return h->v;
+    case 3: return h->grad;
+    default: return nullptr;
+  }
+}
+
+pinn_dd_status pinn_dd_get_params(pinn_dd* h, int32_t sub, int32_t what, float* dst) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  float* src = state_ptr(h, what);
+  if (!src || sub < 0 || sub >= h->d.n_sub || !dst) return fail(h, PINN_DD_EINVAL, "bad get_params arguments");
+  dim3 g((h->n_packed + 255) / 256, 1);
+  k_gather<<<g, 256, 0, h->stream>>>(src + size_t(sub) * h->pstride, h->packmap, h->n_packed, h->pstride,
+                                     h->n_packed, dst, 1);
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_set_params(pinn_dd* h, int32_t sub, int32_t what, const float* src) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  float* dst = state_ptr(h, what);
+  if (!dst || sub < 0 || sub >= h->d.n_sub || !src) return fail(h, PINN_DD_EINVAL, "bad set_params arguments");
+  dim3 g((h->n_packed + 255) / 256, 1);
+  k_scatter<<<g, 256, 0, h->stream>>>(src, h->packmap, h->n_packed, h->pstride, h->n_packed,
+                                      dst + size_t(sub) * h->pstride, 1);
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_get_step(pinn_dd* h, int32_t sub, int32_t* t) {
+  if (!h || !t || sub < 0 || sub >= h->d.n_sub) return fail(h, PINN_DD_EINVAL, "bad get_step arguments");
+  CK(h, cudaMemcpyAsync(t, h->tstep + sub, 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4) {
+  if (!h || !ms4) return fail(h, PINN_DD_EINVAL, "bad kernel_times arguments");
+  CK(h, cudaStreamSynchronize(h->stream));
+  ms4[0] = h->ms[0];
+  ms4[1] = h->ms[1];
+  ms4[2] = h->ms[2];
+  ms4[3] = double(h->launches);
+  h->ms[0] = h->ms[1] = h->ms[2] = 0.0;
+  h->launches = 0;
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_plan_info(pinn_dd* h, int64_t* info4) {
+  if (!h || !info4) return fail(h, PINN_DD_EINVAL, "bad plan_info arguments");
+  info4[0] = h->ops->P;
+  info4[1] = h->tpc;
+  info4[2] = h->n_chunks1;
+  info4[3] = h->grid1;
+  return PINN_DD_OK;
+}
+
+void pinn_dd_destroy(pinn_dd* h) {
+  if (!h) return;
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  delete h;
+}
+
+const char* pinn_dd_last_error(const pinn_dd* h) {
+  if (!h) return g_create_error.c_str();
+  return h->err.c_str();
+}
+
+}  // extern "C"

@@ -1,0 +1,711 @@
+// pinn_dd_kernels.cuh -- the fused kernels (templated on the network shape).
+//
+// K1  k_fused<MODE=0>: one persistent CTA per SM; for every tile of P points of
+//     one subdomain: layer-by-layer forward Taylor jets (weights in SMEM,
+//     pre-activation jets stashed in TMEM), pointwise operator + loss terms +
+//     adjoint seeds (epilogue), reverse sweep through the jets, dW/db/da
+//     partials accumulated per chunk.  Algorithm 1 red stage + J + gradient.
+// K2  k_fused<MODE=1>: forward + payload epilogue at interface points
+//     (Algorithm 1).
+// K5  k_reduce_adam: fixed-order reduction of the chunk partials, J_q assembly
+//     (Eq. 5/6) and the per-subdomain Adam step.
+// K6  k_predict: value-only forward + Eq. (4) stitching.
+#pragma once
+
+#include "pinn_dd_device.cuh"
+
+namespace pinn {
+
+__device__ __forceinline__ void rmw_store(float* p, float v, bool first) {
+  *p = first ? v : (*p + v);
+}
+
+// block-wide sum of R values per thread, fixed order (shuffle tree, then warps 0..3)
+template <int R>
+__device__ __forceinline__ void block_sum(float* v, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float x = v[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    v[r] = x;
+  }
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) red[w * R + r] = v[r];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float s = 0.0f;
+#pragma unroll
+      for (int ww = 0; ww < kThreads / 32; ++ww) s += red[ww * R + r];
+      v[r] = s;
+    }
+  }
+}
+
+template <int N, int NH, int DO>
+__device__ __forceinline__ void load_weights(const float* G, float slope_n, float* sm) {
+  using C = KCfg<N, NH, DO>;
+  using LY = Lay<N, NH, DO>;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 2 * N; e += kThreads) sm[C::oW1 + e] = G[LY::offW(1) + e];
+  for (int e = tid; e < N; e += kThreads) sm[C::oB1 + e] = G[LY::offB(1) + e];
+#pragma unroll 1
+  for (int k = 2; k <= NH; ++k) {
+    const float* W = G + LY::offW(k);
+    float* dst = sm + C::oWh + (k - 2) * C::WROWS;
+    for (int e = tid; e < N * N; e += kThreads) {
+      const int j = e / N, i = e % N;
+      dst[j * C::WS + (j / kJT) * 4 + i] = W[e];
+    }
+    for (int e = tid; e < N; e += kThreads) sm[C::oBh + (k - 2) * N + e] = G[LY::offB(k) + e];
+  }
+  for (int e = tid; e < DO * N; e += kThreads) {
+    const int o = e / N, i = e % N;
+    sm[C::oWo + o * C::WS + i] = G[LY::offW(NH + 1) + e];
+  }
+  for (int e = tid; e < DO; e += kThreads) sm[C::oBo + e] = G[LY::offB(NH + 1) + e];
+  for (int e = tid; e < NH; e += kThreads) sm[C::oSl + e] = slope_n * G[LY::offA(e + 1)];
+}
+
+// forward GEMM of one hidden layer for this thread's (point, neuron block):
+// z[c][jj] = sum_i W[j][i] Hin[i][p].c  (+ b on the value channel)
+template <int N, int NH, int DO>
+__device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const float* __restrict__ W,
+                                         const float* __restrict__ b, float* z, int pg, int nb) {
+  using C = KCfg<N, NH, DO>;
+  const int j0 = nb * kJT;
+#pragma unroll
+  for (int jj = 0; jj < kJT; ++jj) {
+    z[jj] = b[j0 + jj];
+    z[kJT + jj] = 0.0f;
+    z[2 * kJT + jj] = 0.0f;
+    z[3 * kJT + jj] = 0.0f;
+  }
+  const float* Wb = W + j0 * C::WS + nb * 4;
+#pragma unroll 2
+  for (int i = 0; i < N; i += 4) {
+    const float4 h0 = Hin[(i + 0) * C::PSTR + pg];
+    const float4 h1 = Hin[(i + 1) * C::PSTR + pg];
+    const float4 h2 = Hin[(i + 2) * C::PSTR + pg];
+    const float4 h3 = Hin[(i + 3) * C::PSTR + pg];
+#pragma unroll
+    for (int jj = 0; jj < kJT; ++jj) {
+      const float4 w = *reinterpret_cast<const float4*>(Wb + jj * C::WS + i);
+      float a0 = z[jj], a1 = z[kJT + jj], a2 = z[2 * kJT + jj], a3 = z[3 * kJT + jj];
+      a0 = fmaf(w.x, h0.x, a0); a1 = fmaf(w.x, h0.y, a1); a2 = fmaf(w.x, h0.z, a2); a3 = fmaf(w.x, h0.w, a3);
+      a0 = fmaf(w.y, h1.x, a0); a1 = fmaf(w.y, h1.y, a1); a2 = fmaf(w.y, h1.z, a2); a3 = fmaf(w.y, h1.w, a3);
+      a0 = fmaf(w.z, h2.x, a0); a1 = fmaf(w.z, h2.y, a1); a2 = fmaf(w.z, h2.z, a2); a3 = fmaf(w.z, h2.w, a3);
+      a0 = fmaf(w.w, h3.x, a0); a1 = fmaf(w.w, h3.y, a1); a2 = fmaf(w.w, h3.z, a2); a3 = fmaf(w.w, h3.w, a3);
+      z[jj] = a0; z[kJT + jj] = a1; z[2 * kJT + jj] = a2; z[3 * kJT + jj] = a3;
+    }
+  }
+}
+
+// reverse GEMM (input adjoint): hb[c][ii] = sum_j Zb[j][p].c W[j][j0 + ii]
+template <int N, int NH, int DO>
+__device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const float* __restrict__ W, float* hb,
+                                         int pg, int nb) {
+  using C = KCfg<N, NH, DO>;
+  const int j0 = nb * kJT;
+#pragma unroll
+  for (int e = 0; e < kA; ++e) hb[e] = 0.0f;
+#pragma unroll 2
+  for (int j = 0; j < N; ++j) {
+    const float4 zb = Zb[j * C::PSTR + pg];
+    const float* wr = W + j * C::WS + (j / kJT) * 4 + j0;
+#pragma unroll
+    for (int q = 0; q < kJT / 4; ++q) {
+      const float4 w = *reinterpret_cast<const float4*>(wr + 4 * q);
+      const float ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int ii = 4 * q + m;
+        hb[ii] = fmaf(zb.x, ws[m], hb[ii]);
+        hb[kJT + ii] = fmaf(zb.y, ws[m], hb[kJT + ii]);
+        hb[2 * kJT + ii] = fmaf(zb.z, ws[m], hb[2 * kJT + ii]);
+        hb[3 * kJT + ii] = fmaf(zb.w, ws[m], hb[3 * kJT + ii]);
+      }
+    }
+  }
+}
+
+// weight gradient of one hidden layer (mapping B):
+// dW[j][i] += sum_p sum_c Zb[j][p].c H[i][p].c, rows/cols interleaved per thread.
+template <int N, int NH, int DO>
+__device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const float4* __restrict__ H, float* dst,
+                                        bool first, float* sDw) {
+  using C = KCfg<N, NH, DO>;
+  constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
+  constexpr int PS = C::P / S;
+  const int tid = threadIdx.x;
+  if (tid < NBLK * S) {
+    const int r = tid % NBLK, s = tid / NBLK;
+    const int jb = r / NI, ib = r % NI;
+    float acc[JB][IB];
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = 0.0f;
+#pragma unroll 1
+    for (int p = s * PS; p < (s + 1) * PS; ++p) {
+      float4 zr[JB], hr[IB];
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj) zr[jj] = Zb[(jb + NJ * jj) * C::PSTR + p];
+#pragma unroll
+      for (int ii = 0; ii < IB; ++ii) hr[ii] = H[(ib + NI * ii) * C::PSTR + p];
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj)
+#pragma unroll
+        for (int ii = 0; ii < IB; ++ii) {
+          float a = acc[jj][ii];
+          a = fmaf(zr[jj].x, hr[ii].x, a);
+          a = fmaf(zr[jj].y, hr[ii].y, a);
+          a = fmaf(zr[jj].z, hr[ii].z, a);
+          a = fmaf(zr[jj].w, hr[ii].w, a);
+          acc[jj][ii] = a;
+        }
+    }
+    if constexpr (S == 1) {
+      float old[JB][IB];
+      if (!first) {
+#pragma unroll
+        for (int jj = 0; jj < JB; ++jj)
+#pragma unroll
+          for (int ii = 0; ii < IB; ++ii) old[jj][ii] = dst[(jb + NJ * jj) * N + ib + NI * ii];
+      }
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj)
+#pragma unroll
+        for (int ii = 0; ii < IB; ++ii)
+          dst[(jb + NJ * jj) * N + ib + NI * ii] = first ? acc[jj][ii] : old[jj][ii] + acc[jj][ii];
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj)
+#pragma unroll
+        for (int ii = 0; ii < IB; ++ii) sDw[(s * NBLK + r) * JB * IB + jj * IB + ii] = acc[jj][ii];
+    }
+  }
+  if constexpr (S > 1) {
+    __syncthreads();
+    for (int e = tid; e < NBLK * JB * IB; e += kThreads) {
+      const int r = e / (JB * IB), jj = (e % (JB * IB)) / IB, ii = e % IB;
+      float v = 0.0f;
+#pragma unroll
+      for (int s = 0; s < S; ++s) v += sDw[(s * NBLK + r) * JB * IB + jj * IB + ii];
+      const int jb = r / NI, ib = r % NI;
+      rmw_store(dst + (jb + NJ * jj) * N + ib + NI * ii, v, first);
+    }
+  }
+}
+
+__device__ __forceinline__ float4 f4(const float* v, int jj) {
+  return make_float4(v[jj], v[kJT + jj], v[2 * kJT + jj], v[3 * kJT + jj]);
+}
+__device__ __forceinline__ void st4(float* v, int jj, float4 x) {
+  v[jj] = x.x; v[kJT + jj] = x.y; v[2 * kJT + jj] = x.z; v[3 * kJT + jj] = x.w;
+}
+
+template <int N, int NH, int DO, int ACT, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
+  using C = KCfg<N, NH, DO>;
+  using LY = Lay<N, NH, DO>;
+  extern __shared__ __align__(16) float sm[];
+  const int tid = threadIdx.x;
+  const int nb = tid % C::NB, pg = tid / C::NB;
+  const int j0 = nb * kJT;
+  const float* sW1 = sm + C::oW1;
+  const float* sB1 = sm + C::oB1;
+  const float* sWh = sm + C::oWh;
+  const float* sBh = sm + C::oBh;
+  const float* sWo = sm + C::oWo;
+  const float* sBo = sm + C::oBo;
+  const float* sSl = sm + C::oSl;
+  float4* buf0 = reinterpret_cast<float4*>(sm + C::oBuf);
+  float4* buf1 = buf0 + N * C::PSTR;
+  float4* sU = reinterpret_cast<float4*>(sm + C::oU);
+  float* sX = sm + C::oX;
+  float* sY = sX + C::P;
+  float* sRed = sm + C::oRed;
+  float* sDw = sm + C::oDw;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::TOTAL - 4);
+  const float m1 = a.m1, m2 = a.m2;
+  constexpr int NF = DO + (DO == 3 ? 3 : 1);
+
+  Stash st;
+  st.tid = tid;
+  st.g = nullptr;
+  st.taddr = 0;
+  if constexpr (MODE == 0) {
+    if (a.gstash == nullptr) {
+      if (tid < 32) tmem_alloc512(tslot);
+      tmem_fence_before();
+      __syncthreads();
+      tmem_fence_after();
+      st.taddr = *tslot + (uint32_t((tid >> 5) * 32) << 16);
+    } else {
+      st.g = a.gstash + size_t(blockIdx.x) * NH * kA * kThreads;
+    }
+  }
+
+  int cur_sub = -1;
+#pragma unroll 1
+  for (int c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    const Chunk ch = a.chunks[c];
+    if (ch.sub != cur_sub) {
+      __syncthreads();
+      load_weights<N, NH, DO>(a.params + size_t(ch.sub) * a.pstride, a.slope_n, sm);
+      cur_sub = ch.sub;
+    }
+    const float4 lw = a.sub_w[ch.sub];
+    float* Pc = a.partial + size_t(c) * a.pstride;
+    const int ntiles = (ch.count + C::P - 1) / C::P;
+#pragma unroll 1
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t p0 = int64_t(ch.start) + int64_t(t) * C::P;
+      const int np = min(C::P, ch.count - t * C::P);
+      const bool first = (t == 0);
+      __syncthreads();
+      for (int p = tid; p < C::P; p += kThreads) {
+        float x = 0.0f, y = 0.0f;
+        if (p < np) {
+          x = a.coords[p0 + p];
+          y = a.coords[a.n_points + p0 + p];
+        }
+        sX[p] = x;
+        sY[p] = y;
+      }
+      __syncthreads();
+
+      // ------------------------------------------------------------ forward
+      float z[kA];
+      {
+        const float x = sX[pg], y = sY[pg];
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) {
+          const int j = j0 + jj;
+          const float w0 = sW1[2 * j], w1 = sW1[2 * j + 1];
+          z[jj] = fmaf(w0, x, fmaf(w1, y, sB1[j]));   // z = W^1 x + b^1
+          z[kJT + jj] = w0;                           // dz/dx1 = W^1[:,0]
+          z[2 * kJT + jj] = w1;                       // dz/dx2 = W^1[:,1]
+          z[3 * kJT + jj] = 0.0f;                     // Delta z = 0
+        }
+        if constexpr (MODE == 0) st.store(0, z);
+        const float s = sSl[0];
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int k = 2; k <= NH; ++k) {
+        const float4* Hin = (k & 1) ? buf1 : buf0;
+        float4* Hout = (k & 1) ? buf0 : buf1;
+        gemm_fwd<N, NH, DO>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
+        if constexpr (MODE == 0) st.store(k - 1, z);
+        const float s = sSl[k - 1];
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
+        __syncthreads();
+      }
+      const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
+      for (int idx = tid; idx < C::P * DO; idx += kThreads) {
+        const int p = idx % C::P, o = idx / C::P;
+        float4 acc = make_float4(sBo[o], 0.0f, 0.0f, 0.0f);
+        const float* w = sWo + o * C::WS;
+#pragma unroll 4
+        for (int i = 0; i < N; ++i) {
+          const float4 h = HL[i * C::PSTR + p];
+          const float wi = w[i];
+          acc.x = fmaf(wi, h.x, acc.x);
+          acc.y = fmaf(wi, h.y, acc.y);
+          acc.z = fmaf(wi, h.z, acc.z);
+          acc.w = fmaf(wi, h.w, acc.w);
+        }
+        sU[p * DO + o] = acc;
+      }
+      __syncthreads();
+
+      // ----------------------------------------------------------- epilogue
+      if constexpr (MODE == 1) {
+        // payload: u(x_I) and f.n (cPINN) or F (XPINN) (Algorithm 1)
+        for (int p = tid; p < np; p += kThreads) {
+          const int64_t gp = p0 + p;
+          float4 U[DO];
+#pragma unroll
+          for (int o = 0; o < DO; ++o) U[o] = sU[p * DO + o];
+          float r[3];
+          float dr[3][DO][4];
+          int ne;
+          if (a.method == 1) {
+            const float2 n = a.seg_normal[a.pinfo[gp] >> 2];
+            ne = pde_flux<DO>(a.pc, U, sX[p], sY[p], n.x, n.y, r, dr);
+          } else {
+            ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);
+          }
+          float* q = a.payload + size_t(gp) * NF;
+#pragma unroll
+          for (int o = 0; o < DO; ++o) q[o] = U[o].x;
+          for (int e = 0; e < ne; ++e) q[DO + e] = r[e];
+        }
+        continue;
+      } else {
+        float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // MSE_u, MSE_F, MSE_uavg, MSE_if partials
+        for (int p = tid; p < C::P; p += kThreads) {
+          float4 U[DO], Ub[DO];
+#pragma unroll
+          for (int o = 0; o < DO; ++o) {
+            U[o] = sU[p * DO + o];
+            Ub[o] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          }
+          if (p < np) {
+            const int64_t gp = p0 + p;
+            const int info = a.pinfo[gp];
+            const int kind = info & 3;
+            const float inv = a.pinv[gp];
+            float r[3];
+            float dr[3][DO][4];
+            if (kind == 0) {
+              // residual point: W_F (1/N_F) sum_e F_e^2
+              const int ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);
+              for (int e = 0; e < ne; ++e) {
+                lsum[1] += inv * r[e] * r[e];
+                const float cf = 2.0f * lw.y * inv * r[e];
+#pragma unroll
+                for (int o = 0; o < DO; ++o) {
+                  Ub[o].x = fmaf(cf, dr[e][o][0], Ub[o].x);
+                  Ub[o].y = fmaf(cf, dr[e][o][1], Ub[o].y);
+                  Ub[o].z = fmaf(cf, dr[e][o][2], Ub[o].z);
+                  Ub[o].w = fmaf(cf, dr[e][o][3], Ub[o].w);
+                }
+              }
+            } else if (kind == 1) {
+              // training point: W_u (1/N_u) sum_o mask_o |u^(i)_o - u_o|^2
+#pragma unroll
+              for (int o = 0; o < DO; ++o) {
+                const float m = a.mask[size_t(o) * a.n_points + gp];
+                const float d = m * (U[o].x - a.target[size_t(o) * a.n_points + gp]);
+                lsum[0] += inv * d * d;
+                Ub[o].x += 2.0f * lw.x * inv * d;
+              }
+            } else {
+              // interface point: neighbour payload is a constant
+              const float* q = a.payload + size_t(a.ptwin[gp]) * NF;
+#pragma unroll
+              for (int o = 0; o < DO; ++o) {
+                const float d = U[o].x - q[o];   // u_q - {{u}} = d / 2  (Z1)
+                lsum[2] += inv * 0.25f * d * d;
+                Ub[o].x += 0.5f * lw.z * inv * d;
+              }
+              int ne;
+              if (a.method == 1) {
+                const float2 n = a.seg_normal[info >> 2];
+                ne = pde_flux<DO>(a.pc, U, sX[p], sY[p], n.x, n.y, r, dr);
+              } else {
+                ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);
+              }
+              for (int e = 0; e < ne; ++e) {
+                const float d = r[e] - q[DO + e];
+                lsum[3] += inv * d * d;
+                const float cf = 2.0f * lw.w * inv * d;
+#pragma unroll
+                for (int o = 0; o < DO; ++o) {
+                  Ub[o].x = fmaf(cf, dr[e][o][0], Ub[o].x);
+                  Ub[o].y = fmaf(cf, dr[e][o][1], Ub[o].y);
+                  Ub[o].z = fmaf(cf, dr[e][o][2], Ub[o].z);
+                  Ub[o].w = fmaf(cf, dr[e][o][3], Ub[o].w);
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
+        }
+        __syncthreads();
+
+        // ------------------------------------------------------------ reverse
+        // output layer: dW^L, db^L
+        for (int idx = tid; idx < DO * N; idx += kThreads) {
+          const int o = idx / N, i = idx % N;
+          float acc = 0.0f;
+#pragma unroll 4
+          for (int p = 0; p < C::P; ++p) {
+            const float4 h = HL[i * C::PSTR + p];
+            const float4 ub = sU[p * DO + o];
+            acc = fmaf(h.x, ub.x, fmaf(h.y, ub.y, fmaf(h.z, ub.z, fmaf(h.w, ub.w, acc))));
+          }
+          rmw_store(Pc + LY::offW(NH + 1) + idx, acc, first);
+        }
+        if (tid < DO) {
+          float acc = 0.0f;
+          for (int p = 0; p < C::P; ++p) acc += sU[p * DO + tid].x;
+          rmw_store(Pc + LY::offB(NH + 1) + tid, acc, first);
+        }
+        float sbar[NH];
+#pragma unroll
+        for (int k = 0; k < NH; ++k) sbar[k] = 0.0f;
+        float hb[kA];
+#pragma unroll
+        for (int e = 0; e < kA; ++e) hb[e] = 0.0f;
+#pragma unroll
+        for (int o = 0; o < DO; ++o) {
+          const float4 ub = sU[pg * DO + o];
+#pragma unroll
+          for (int jj = 0; jj < kJT; ++jj) {
+            const float w = sWo[o * C::WS + j0 + jj];
+            hb[jj] = fmaf(ub.x, w, hb[jj]);
+            hb[kJT + jj] = fmaf(ub.y, w, hb[kJT + jj]);
+            hb[2 * kJT + jj] = fmaf(ub.z, w, hb[2 * kJT + jj]);
+            hb[3 * kJT + jj] = fmaf(ub.w, w, hb[3 * kJT + jj]);
+          }
+        }
+        {
+          st.load(NH - 1, z);
+          const float s = sSl[NH - 1];
+          float sb = 0.0f;
+#pragma unroll
+          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, sb));
+          sbar[NH - 1] += sb;
+          if (NH >= 2) {
+            st.load(NH - 2, z);
+            const float s2 = sSl[NH - 2];
+#pragma unroll
+            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2));
+          }
+        }
+        float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
+        float4* bufH = buf1;   // activation of the layer below
+        __syncthreads();
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) {
+          bufZ[(j0 + jj) * C::PSTR + pg] = f4(hb, jj);
+          if (NH >= 2) bufH[(j0 + jj) * C::PSTR + pg] = f4(z, jj);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int k = NH; k >= 2; --k) {
+          // dW^k, db^k
+          gemm_dw<N, NH, DO>(bufZ, bufH, Pc + LY::offW(k), first, sDw);
+          for (int j = tid; j < N; j += kThreads) {
+            float acc = 0.0f;
+#pragma unroll 4
+            for (int p = 0; p < C::P; ++p) acc += bufZ[j * C::PSTR + p].x;
+            rmw_store(Pc + LY::offB(k) + j, acc, first);
+          }
+          // adjoint of H^{k-1}, then of Z^{k-1}
+          gemm_bwd<N, NH, DO>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
+          st.load(k - 2, z);
+          const float s = sSl[k - 2];
+          float sb = 0.0f;
+#pragma unroll
+          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, sb));
+#pragma unroll
+          for (int kk = 0; kk < NH; ++kk)
+            if (kk == k - 2) sbar[kk] += sb;
+          const bool more = (k - 1 >= 2);
+          if (more) {
+            st.load(k - 3, z);
+            const float s2 = sSl[k - 3];
+#pragma unroll
+            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2));
+          }
+          __syncthreads();
+#pragma unroll
+          for (int jj = 0; jj < kJT; ++jj) {
+            bufZ[(j0 + jj) * C::PSTR + pg] = f4(hb, jj);
+            if (more) bufH[(j0 + jj) * C::PSTR + pg] = f4(z, jj);
+          }
+          __syncthreads();
+        }
+        // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
+        for (int j = tid; j < N; j += kThreads) {
+          float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
+#pragma unroll 4
+          for (int p = 0; p < C::P; ++p) {
+            const float4 zb = bufZ[j * C::PSTR + p];
+            a0 = fmaf(zb.x, sX[p], a0) + zb.y;
+            a1 = fmaf(zb.x, sY[p], a1) + zb.z;
+            ab += zb.x;
+          }
+          rmw_store(Pc + LY::offW(1) + 2 * j, a0, first);
+          rmw_store(Pc + LY::offW(1) + 2 * j + 1, a1, first);
+          rmw_store(Pc + LY::offB(1) + j, ab, first);
+        }
+        // slopes (da^k = n dJ/ds_k) and loss partials
+        float red[NH + 4];
+#pragma unroll
+        for (int k = 0; k < NH; ++k) red[k] = a.slope_n * sbar[k];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) red[NH + r] = lsum[r];
+        block_sum<NH + 4>(red, sRed);
+        if (tid == 0) {
+#pragma unroll
+          for (int k = 0; k < NH; ++k) rmw_store(Pc + LY::offA(k + 1), red[k], first);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) rmw_store(a.partial_loss + size_t(c) * 4 + r, red[NH + r], first);
+        }
+      }
+    }
+  }
+  if constexpr (MODE == 0) {
+    if (a.gstash == nullptr) {
+      __syncthreads();
+      tmem_fence_after();
+      if (tid < 32) tmem_dealloc512(*tslot);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// K5: gradient reduction over chunk partials (fixed order), J assembly, Adam.
+// mode 0: reduce only; 1: reduce + Adam; 2: Adam on the stored gradient.
+// ----------------------------------------------------------------------------
+struct RArgs {
+  const float* partial;
+  const float* partial_loss;
+  const int32_t* sub_chunk;   // [n_sub+1]
+  int pstride;
+  float* grad;                // [n_sub][pstride]
+  float* params;
+  float* m;
+  float* v;
+  int32_t* tstep;             // [n_sub]
+  int32_t* done;              // [n_sub] block counters
+  const float4* sub_w;        // loss weights
+  const float4* sub_adam;     // lr, beta1, beta2, eps
+  float* loss;                // [n_sub][8]
+  int32_t* flag;              // non-finite flag
+  int mode;
+};
+
+__global__ void k_reduce_adam(const RArgs r) {
+  const int q = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c0 = r.sub_chunk[q], c1 = r.sub_chunk[q + 1];
+  const int t = r.tstep[q] + 1;
+  if (i < r.pstride) {
+    float g;
+    if (r.mode == 2) {
+      g = r.grad[size_t(q) * r.pstride + i];
+    } else {
+      g = 0.0f;
+      for (int c = c0; c < c1; ++c) g += r.partial[size_t(c) * r.pstride + i];
+      r.grad[size_t(q) * r.pstride + i] = g;
+    }
+    if (!isfinite(g)) atomicOr(r.flag, 2);
+    if (r.mode != 0) {
+      const float4 ad = r.sub_adam[q];
+      const size_t k = size_t(q) * r.pstride + i;
+      const float mm = ad.y * r.m[k] + (1.0f - ad.y) * g;
+      const float vv = ad.z * r.v[k] + (1.0f - ad.z) * g * g;
+      r.m[k] = mm;
+      r.v[k] = vv;
+      const float mh = mm / (1.0f - powf(ad.y, float(t)));
+      const float vh = vv / (1.0f - powf(ad.z, float(t)));
+      r.params[k] -= ad.x * mh / (sqrtf(vh) + ad.w);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && r.mode != 2) {
+    float l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int c = c0; c < c1; ++c)
+      for (int e = 0; e < 4; ++e) l[e] += r.partial_loss[size_t(c) * 4 + e];
+    const float4 w = r.sub_w[q];
+    const float J = w.x * l[0] + w.y * l[1] + w.z * l[2] + w.w * l[3];
+    float* L = r.loss + size_t(q) * 8;
+    L[0] = l[0]; L[1] = l[1]; L[2] = l[2]; L[3] = l[3]; L[4] = J;
+    L[5] = isfinite(J) ? 0.0f : 1.0f;
+    L[6] = 0.0f; L[7] = 0.0f;
+    if (!isfinite(J)) atomicOr(r.flag, 1);
+  }
+  if (r.mode != 0) {
+    // the last block of subdomain q advances its Adam step counter
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int prev = atomicAdd(&r.done[q], 1);
+      if (prev == int(gridDim.x) - 1) {
+        r.tstep[q] = t;
+        r.done[q] = 0;
+        __threadfence();
+      }
+    }
+  }
+}
+
+// packed <-> internal parameter layout
+__global__ void k_gather(const float* src, const int32_t* map, int n, int pstride, int sub_stride_dst,
+                         float* dst, int n_sub) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;
+  if (i < n && q < n_sub) dst[size_t(q) * sub_stride_dst + i] = src[size_t(q) * pstride + map[i]];
+}
+__global__ void k_scatter(const float* src, const int32_t* map, int n, int pstride, int sub_stride_src,
+                          float* dst, int n_sub) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;
+  if (i < n && q < n_sub) dst[size_t(q) * pstride + map[i]] = src[size_t(q) * sub_stride_src + i];
+}
+
+// ----------------------------------------------------------------------------
+// K6: value-only forward + Eq. (4) stitching
+// ----------------------------------------------------------------------------
+template <int N, int NH, int DO, int ACT>
+__global__ void k_predict(const float* params, int pstride, float slope_n, const float* pts, const int32_t* owners,
+                          int64_t n, float* out) {
+  using LY = Lay<N, NH, DO>;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float x = pts[p], y = pts[n + p];
+  float acc[DO];
+#pragma unroll
+  for (int o = 0; o < DO; ++o) acc[o] = 0.0f;
+  int S = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int q = owners[p * 4 + k];
+    if (q < 0) continue;
+    ++S;
+    const float* G = params + size_t(q) * pstride;
+    float h[N], g[N];
+    float s = slope_n * G[LY::offA(1)];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      float s0, s1, s2, s3;
+      act_derivs<ACT>(s * (G[2 * j] * x + G[2 * j + 1] * y + G[LY::offB(1) + j]), s0, s1, s2, s3);
+      h[j] = s0;
+    }
+    for (int l = 2; l <= NH; ++l) {
+      s = slope_n * G[LY::offA(l)];
+      const float* W = G + LY::offW(l);
+      const float* b = G + LY::offB(l);
+      for (int j = 0; j < N; ++j) {
+        float zz = b[j];
+#pragma unroll
+        for (int i = 0; i < N; ++i) zz = fmaf(W[j * N + i], h[i], zz);
+        g[j] = zz;
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        float s0, s1, s2, s3;
+        act_derivs<ACT>(s * g[j], s0, s1, s2, s3);
+        h[j] = s0;
+      }
+    }
+    const float* W = G + LY::offW(NH + 1);
+#pragma unroll
+    for (int o = 0; o < DO; ++o) {
+      float u = G[LY::offB(NH + 1) + o];
+#pragma unroll
+      for (int i = 0; i < N; ++i) u = fmaf(W[o * N + i], h[i], u);
+      acc[o] += u;
+    }
+  }
+  const float inv = S > 0 ? 1.0f / float(S) : 0.0f;   // indicator 1/S
+#pragma unroll
+  for (int o = 0; o < DO; ++o) out[size_t(o) * n + p] = acc[o] * inv;
+}
+
+}  // namespace pinn
