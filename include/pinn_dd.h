@@ -191,6 +191,11 @@ pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4);
    number of chunks, grid size}. */
 pinn_dd_status pinn_dd_plan_info(pinn_dd* h, int64_t* info4);
 
+/* Debug / test access to internal device buffers (library-owned, read-only
+   for the caller): 0 point class word, 1 1/N per point, 2 twin row, 3 K1
+   chunks, 4 K2 chunks, 5 gradient partials, 6 internal (padded) parameters. */
+pinn_dd_status pinn_dd_debug_buffer(pinn_dd* h, int32_t which, void** ptr, int64_t* bytes);
+
 void pinn_dd_destroy(pinn_dd* h);
 
 /* Message of the last failing call on h (NULL h: the last pinn_dd_create /

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpinn_dd.so")
+LIB_PATH = os.environ.get("PINN_DD_LIB", os.path.join(_HERE, "libpinn_dd.so"))
 
 OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, ENONFINITE, EPROTOCOL = range(7)
 METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2}
@@ -31,7 +31,7 @@ EXPORTS = [
     "pinn_dd_n_params", "pinn_dd_workspace_size", "pinn_dd_create", "pinn_dd_interface_payload",
     "pinn_dd_payload_buffer", "pinn_dd_loss_grad", "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict",
     "pinn_dd_get_params", "pinn_dd_set_params", "pinn_dd_get_step", "pinn_dd_kernel_times",
-    "pinn_dd_plan_info", "pinn_dd_destroy", "pinn_dd_last_error",
+    "pinn_dd_plan_info", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
 ]
 
 
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH):
     lib.pinn_dd_get_step.argtypes = [vp, i32, C.POINTER(i32)]
     lib.pinn_dd_kernel_times.argtypes = [vp, C.POINTER(C.c_double)]
     lib.pinn_dd_plan_info.argtypes = [vp, C.POINTER(i64)]
+    lib.pinn_dd_debug_buffer.argtypes = [vp, i32, C.POINTER(vp), C.POINTER(i64)]
     lib.pinn_dd_destroy.argtypes = [vp]
     lib.pinn_dd_destroy.restype = None
     lib.pinn_dd_last_error.argtypes = [vp]
@@ -355,6 +356,13 @@ class PinnDD:
         ms = (C.c_double * 4)()
         self._check(self.lib.pinn_dd_kernel_times(self.h, ms))
         return list(ms)
+
+    def debug_buffer(self, which: int, dtype=torch.int32) -> torch.Tensor:
+        """Copy of an internal device buffer (tests / debugging)."""
+        ptr, nb = C.c_void_p(), C.c_int64()
+        self._check(self.lib.pinn_dd_debug_buffer(self.h, which, C.byref(ptr), C.byref(nb)))
+        off = ptr.value - self.workspace.data_ptr()
+        return self.workspace[off: off + nb.value].view(dtype).clone()
 
     def plan_info(self):
         v = (C.c_int64 * 4)()

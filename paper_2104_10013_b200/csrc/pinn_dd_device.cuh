@@ -29,19 +29,47 @@ __host__ __device__ constexpr int al4(int x) { return (x + 3) & ~3; }
 // [2, N x NH, DO]; the packed layout of the ABI is W1 b1 a1 W2 b2 a2 ... WL bL.
 template <int N, int NH, int DO>
 struct Lay {
+  // Closed forms (no recursion: a recursive constexpr evaluated with a runtime
+  // layer index compiles to a recursive device CALL, which clobbers the warp
+  // convergence-barrier registers and leaves warps diverged at bar.sync).
   static constexpr int L = NH + 1;
+  static constexpr int H1 = al4(al4(2 * N) + N) + 4;          // start of W^2
+  static constexpr int SH = al4(N * N) + al4(N) + 4;          // one hidden layer block
   __host__ __device__ static constexpr int nin(int k) { return k == 1 ? 2 : N; }
   __host__ __device__ static constexpr int nout(int k) { return k == L ? DO : N; }
-  __host__ __device__ static constexpr int offW(int k) { return k == 1 ? 0 : al4(offA(k - 1) + 1); }
-  __host__ __device__ static constexpr int offB(int k) { return al4(offW(k) + nout(k) * nin(k)); }
-  __host__ __device__ static constexpr int offA(int k) { return al4(offB(k) + nout(k)); }
+  __host__ __device__ static constexpr int offW(int k) { return k == 1 ? 0 : H1 + (k - 2) * SH; }
+  __host__ __device__ static constexpr int offB(int k) {
+    return k == 1 ? al4(2 * N) : offW(k) + al4(nout(k) * N);
+  }
+  __host__ __device__ static constexpr int offA(int k) { return offB(k) + al4(N); }
   __host__ __device__ static constexpr int total() { return al4(offB(L) + DO); }
 };
+
+// recursive reference definition, checked at compile time against the closed forms
+template <int N, int NH, int DO>
+struct LayRef {
+  static constexpr int L = NH + 1;
+  static constexpr int nin(int k) { return k == 1 ? 2 : N; }
+  static constexpr int nout(int k) { return k == L ? DO : N; }
+  static constexpr int offW(int k) { return k == 1 ? 0 : al4(offA(k - 1) + 1); }
+  static constexpr int offB(int k) { return al4(offW(k) + nout(k) * nin(k)); }
+  static constexpr int offA(int k) { return al4(offB(k) + nout(k)); }
+};
+template <int N, int NH, int DO>
+constexpr bool lay_ok() {
+  for (int k = 1; k <= NH + 1; ++k) {
+    if (Lay<N, NH, DO>::offW(k) != LayRef<N, NH, DO>::offW(k)) return false;
+    if (Lay<N, NH, DO>::offB(k) != LayRef<N, NH, DO>::offB(k)) return false;
+    if (k <= NH && Lay<N, NH, DO>::offA(k) != LayRef<N, NH, DO>::offA(k)) return false;
+  }
+  return true;
+}
 
 // Kernel geometry for width N (mapping A: thread = (point group pg, neuron block nb)).
 template <int N, int NH, int DO>
 struct KCfg {
   static_assert(N % kJT == 0, "width must be a multiple of 20");
+  static_assert(lay_ok<N, NH, DO>(), "closed-form parameter layout mismatch");
   static constexpr int NB = N / kJT;           // neuron blocks
   static constexpr int P = kThreads / NB;      // points per tile (1 point per thread)
   static constexpr int PSTR = P + 1;           // float4 row stride of activation buffers (odd)
@@ -67,8 +95,8 @@ struct KCfg {
   static constexpr int BUF = N * PSTR * 4;
   static constexpr int oU = oBuf + 2 * BUF;                // [P][DO] float4
   static constexpr int oX = oU + P * DO * 4;               // [2][P]
-  static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [32]
-  static constexpr int oDw = oRed + 32;                    // dW split scratch [S][NBLK][JB*IB] (S>1)
+  static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [4 warps][4]
+  static constexpr int oDw = oRed + 16;                    // dW split scratch [S][NBLK][JB*IB] (S>1)
   static constexpr int DWS = (S > 1) ? S * NBLK * JB * IB : 0;
   static constexpr int TOTAL = al4(oDw + DWS + 4);         // + tmem address slot
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
@@ -111,18 +139,19 @@ __device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2)
 }
 
 // adjoint of act_fwd: given hb = dJ/dh (4 channels) and the stashed z-jets,
-// return zb = dJ/dz (4 channels) and accumulate dJ/ds into sbar.
+// return zb = dJ/dz (4 channels).  The slope gradient is NOT accumulated here:
+// J depends on (s_k, W^k, b^k) only through s_k W^k and s_k b^k, so
+// a_k dJ/da_k = <W^k, dJ/dW^k> + <b^k, dJ/db^k> exactly; K5 evaluates that
+// identity once per step.
 template <int ACT>
-__device__ __forceinline__ float4 act_bwd(float4 z, float4 hb, float s, float m1, float m2, float& sbar) {
+__device__ __forceinline__ float4 act_bwd(float4 z, float4 hb, float s, float m1, float m2) {
   float s0, s1, s2, s3;
   act_derivs<ACT>(s * z.x, s0, s1, s2, s3);
   float Q = m1 * z.y * z.y + m2 * z.z * z.z;
-  // primed adjoints (= adjoint / s); see DESIGN.md "activation adjoint"
   float zb = hb.x * s1 + s * s2 * (hb.y * z.y + hb.z * z.z) + hb.w * (s3 * s * s * Q + s2 * s * z.w);
   float g1 = hb.y * s1 + 2.0f * m1 * hb.w * s2 * s * z.y;
   float g2 = hb.z * s1 + 2.0f * m2 * hb.w * s2 * s * z.z;
   float lb = hb.w * s1;
-  sbar += zb * z.x + g1 * z.y + g2 * z.z + lb * z.w;
   return make_float4(s * zb, s * g1, s * g2, s * lb);
 }
 
@@ -180,6 +209,7 @@ struct Stash {
   int tid;
   __device__ __forceinline__ void store(int slot, const float* v) {
     if (g == nullptr) {
+      __syncwarp();   // tcgen05.st is .sync.aligned: the warp must be converged
 #pragma unroll
       for (int q = 0; q < kA / 16; ++q) tmem_st16(taddr + slot * kA + q * 16, v + q * 16);
       tmem_wait_st();
@@ -190,6 +220,7 @@ struct Stash {
   }
   __device__ __forceinline__ void load(int slot, float* v) {
     if (g == nullptr) {
+      __syncwarp();   // tcgen05.ld is .sync.aligned
 #pragma unroll
       for (int q = 0; q < kA / 16; ++q) tmem_ld16(taddr + slot * kA + q * 16, v + q * 16);
     } else {

@@ -37,6 +37,7 @@ struct Ops {
   void (*k2)(const KArgs&, int grid, size_t smem, cudaStream_t);
   void (*pred)(const float*, int, float, const float*, const int32_t*, int64_t, float*, cudaStream_t);
   void (*packmap)(std::vector<int32_t>&);
+  void (*slopetab)(RArgs&);
   cudaError_t (*setattr)(size_t);
 };
 
@@ -67,6 +68,16 @@ struct Inst {
       if (k <= NH) m.push_back(LY::offA(k));
     }
   }
+  static void slopetab(RArgs& r) {
+    r.n_hidden = NH;
+    for (int k = 1; k <= NH; ++k) {
+      r.offW[k - 1] = LY::offW(k);
+      r.nW[k - 1] = LY::nout(k) * LY::nin(k);
+      r.offB[k - 1] = LY::offB(k);
+      r.nB[k - 1] = LY::nout(k);
+      r.offA[k - 1] = LY::offA(k);
+    }
+  }
   static cudaError_t setattr(size_t sm) {
     cudaError_t e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(sm));
@@ -74,7 +85,8 @@ struct Inst {
     return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   }
   static Ops ops() {
-    return Ops{N, NH, DO, ACT, LY::total(), C::P, smem(), &k1, &k2, &pred, &packmap, &setattr};
+    static_assert(NH <= kMaxHidden, "too many hidden layers");
+    return Ops{N, NH, DO, ACT, LY::total(), C::P, smem(), &k1, &k2, &pred, &packmap, &slopetab, &setattr};
   }
 };
 
@@ -112,8 +124,10 @@ struct pinn_dd {
   float4 *sub_w = nullptr, *sub_adam = nullptr;
   Chunk *chunks1 = nullptr, *chunks2 = nullptr;
   cudaStream_t stream = nullptr;
-  // graph
+  // graph (captured and replayed on an internal stream joined to `stream` by events)
   cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gjoin[2] = {};
   // timing
   cudaEvent_t ev[6] = {};
   double ms[3] = {0, 0, 0};
@@ -335,10 +349,9 @@ RArgs make_rargs(pinn_dd* h, int mode) {
   r.loss = h->loss;
   r.flag = h->flag;
   r.mode = mode;
+  h->ops->slopetab(r);
   return r;
 }
-
-const int kRB = 256;
 
 pinn_dd_status launch_k2(pinn_dd* h) {
   if (h->n_chunks2 == 0) return PINN_DD_OK;
@@ -353,9 +366,18 @@ pinn_dd_status launch_k1(pinn_dd* h) {
   CK(h, cudaGetLastError());
   return PINN_DD_OK;
 }
+// mode 0: reduce + slopes (loss_grad); 1: reduce + slopes + Adam (step);
+// 2: Adam on the stored gradient (pinn_dd_adam)
 pinn_dd_status launch_k5(pinn_dd* h, int mode) {
   dim3 g((h->pstride + kRB - 1) / kRB, h->d.n_sub);
-  k_reduce_adam<<<g, kRB, 0, h->stream>>>(make_rargs(h, mode));
+  if (mode != 2) {
+    k_reduce<<<g, kRB, 0, h->stream>>>(make_rargs(h, 0));
+    ++h->launches;
+    CK(h, cudaGetLastError());
+  }
+  RArgs r = make_rargs(h, mode == 0 ? 0 : 1);
+  if (mode == 2) r.n_hidden = 0;   // slopes were filled by pinn_dd_loss_grad
+  k_slope_adam<<<g, kRB, 0, h->stream>>>(r);
   ++h->launches;
   CK(h, cudaGetLastError());
   return PINN_DD_OK;
@@ -570,6 +592,8 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
     CKC(cudaGetLastError());
   }
   for (auto& e : h->ev) CKC(cudaEventCreate(&e));
+  for (auto& e : h->gjoin) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CKC(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
   CKC(cudaStreamSynchronize(st));   // host vectors above go out of scope
   *out = h;
   return PINN_DD_OK;
@@ -623,17 +647,28 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
       if (!h->gexec) {
         cudaGraph_t g;
         const long long before = h->launches;
-        CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t user = h->stream;
+        h->stream = h->gstream;
+        cudaError_t e0 = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+        if (e0 != cudaSuccess) {
+          h->stream = user;
+          return fail(h, PINN_DD_ECUDA, "graph capture: %s", cudaGetErrorString(e0));
+        }
         pinn_dd_status cs = one_iteration(h, false);
         cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+        h->stream = user;
         if (cs != PINN_DD_OK) return cs;
         if (e != cudaSuccess) return fail(h, PINN_DD_ECUDA, "graph capture: %s", cudaGetErrorString(e));
         CK(h, cudaGraphInstantiate(&h->gexec, g, 0));
         cudaGraphDestroy(g);
         h->launches = before;   // counted on every replay below
       }
-      CK(h, cudaGraphLaunch(h->gexec, h->stream));
-      h->launches += (h->n_chunks2 > 0 ? 3 : 2);
+      CK(h, cudaEventRecord(h->gjoin[0], h->stream));
+      CK(h, cudaStreamWaitEvent(h->gstream, h->gjoin[0], 0));
+      CK(h, cudaGraphLaunch(h->gexec, h->gstream));
+      CK(h, cudaEventRecord(h->gjoin[1], h->gstream));
+      CK(h, cudaStreamWaitEvent(h->stream, h->gjoin[1], 0));
+      h->launches += (h->n_chunks2 > 0 ? 4 : 3);
     } else if ((s = one_iteration(h, timed)) != PINN_DD_OK) {
       return s;
     }
@@ -723,11 +758,30 @@ pinn_dd_status pinn_dd_plan_info(pinn_dd* h, int64_t* info4) {
   return PINN_DD_OK;
 }
 
+pinn_dd_status pinn_dd_debug_buffer(pinn_dd* h, int32_t which, void** ptr, int64_t* bytes) {
+  if (!h || !ptr || !bytes) return fail(h, PINN_DD_EINVAL, "bad debug_buffer arguments");
+  const int64_t np = h->d.n_points + 1, ns = h->d.n_sub;
+  switch (which) {
+    case 0: *ptr = h->pinfo; *bytes = np * 4; break;
+    case 1: *ptr = h->pinv; *bytes = np * 4; break;
+    case 2: *ptr = h->ptwin; *bytes = np * 4; break;
+    case 3: *ptr = h->chunks1; *bytes = int64_t(h->n_chunks1) * sizeof(Chunk); break;
+    case 4: *ptr = h->chunks2; *bytes = int64_t(h->n_chunks2) * sizeof(Chunk); break;
+    case 5: *ptr = h->partial; *bytes = int64_t(h->n_chunks1) * h->pstride * 4; break;
+    case 6: *ptr = h->params; *bytes = ns * h->pstride * 4; break;
+    default: return fail(h, PINN_DD_EINVAL, "unknown debug buffer %d", which);
+  }
+  return PINN_DD_OK;
+}
+
 void pinn_dd_destroy(pinn_dd* h) {
   if (!h) return;
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : h->gjoin)
+    if (e) cudaEventDestroy(e);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
   delete h;
 }
 

@@ -16,31 +16,37 @@
 
 namespace pinn {
 
+// CTA barrier preceded by an explicit warp reconvergence.
+__device__ __forceinline__ void cta_sync() {
+  __syncwarp();
+  __syncthreads();
+}
+
 __device__ __forceinline__ void rmw_store(float* p, float v, bool first) {
   *p = first ? v : (*p + v);
 }
 
 // block-wide sum of R values per thread, fixed order (shuffle tree, then warps 0..3)
-template <int R>
-__device__ __forceinline__ void block_sum(float* v, float* red) {
+template <int R, class T>
+__device__ __forceinline__ void block_sum(T* v, T* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    float x = v[r];
+    T x = v[r];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     v[r] = x;
   }
-  __syncthreads();
+  cta_sync();
   if (lane == 0) {
 #pragma unroll
     for (int r = 0; r < R; ++r) red[w * R + r] = v[r];
   }
-  __syncthreads();
+  cta_sync();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      float s = 0.0f;
+      T s = T(0);
 #pragma unroll
       for (int ww = 0; ww < kThreads / 32; ++ww) s += red[ww * R + r];
       v[r] = s;
@@ -192,7 +198,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
     }
   }
   if constexpr (S > 1) {
-    __syncthreads();
+    cta_sync();
     for (int e = tid; e < NBLK * JB * IB; e += kThreads) {
       const int r = e / (JB * IB), jj = (e % (JB * IB)) / IB, ii = e % IB;
       float v = 0.0f;
@@ -243,9 +249,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
   st.taddr = 0;
   if constexpr (MODE == 0) {
     if (a.gstash == nullptr) {
-      if (tid < 32) tmem_alloc512(tslot);
+      if (tid < 32) {
+        __syncwarp();
+        tmem_alloc512(tslot);
+      }
       tmem_fence_before();
-      __syncthreads();
+      cta_sync();
       tmem_fence_after();
       st.taddr = *tslot + (uint32_t((tid >> 5) * 32) << 16);
     } else {
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
   for (int c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
     const Chunk ch = a.chunks[c];
     if (ch.sub != cur_sub) {
-      __syncthreads();
+      cta_sync();
       load_weights<N, NH, DO>(a.params + size_t(ch.sub) * a.pstride, a.slope_n, sm);
       cur_sub = ch.sub;
     }
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       const int64_t p0 = int64_t(ch.start) + int64_t(t) * C::P;
       const int np = min(C::P, ch.count - t * C::P);
       const bool first = (t == 0);
-      __syncthreads();
+      cta_sync();
       for (int p = tid; p < C::P; p += kThreads) {
         float x = 0.0f, y = 0.0f;
         if (p < np) {
@@ -280,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         sX[p] = x;
         sY[p] = y;
       }
-      __syncthreads();
+      cta_sync();
 
       // ------------------------------------------------------------ forward
       float z[kA];
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
       }
-      __syncthreads();
+      cta_sync();
 #pragma unroll 1
       for (int k = 2; k <= NH; ++k) {
         const float4* Hin = (k & 1) ? buf1 : buf0;
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         const float s = sSl[k - 1];
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
-        __syncthreads();
+        cta_sync();
       }
       const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
       for (int idx = tid; idx < C::P * DO; idx += kThreads) {
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         }
         sU[p * DO + o] = acc;
       }
-      __syncthreads();
+      cta_sync();
 
       // ----------------------------------------------------------- epilogue
       if constexpr (MODE == 1) {
@@ -425,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 #pragma unroll
           for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
         }
-        __syncthreads();
+        cta_sync();
 
         // ------------------------------------------------------------ reverse
         // output layer: dW^L, db^L
@@ -445,9 +454,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           for (int p = 0; p < C::P; ++p) acc += sU[p * DO + tid].x;
           rmw_store(Pc + LY::offB(NH + 1) + tid, acc, first);
         }
-        float sbar[NH];
-#pragma unroll
-        for (int k = 0; k < NH; ++k) sbar[k] = 0.0f;
         float hb[kA];
 #pragma unroll
         for (int e = 0; e < kA; ++e) hb[e] = 0.0f;
@@ -466,10 +472,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         {
           st.load(NH - 1, z);
           const float s = sSl[NH - 1];
-          float sb = 0.0f;
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, sb));
-          sbar[NH - 1] += sb;
+          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2));
           if (NH >= 2) {
             st.load(NH - 2, z);
             const float s2 = sSl[NH - 2];
@@ -479,13 +483,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         }
         float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
         float4* bufH = buf1;   // activation of the layer below
-        __syncthreads();
+        cta_sync();
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) {
           bufZ[(j0 + jj) * C::PSTR + pg] = f4(hb, jj);
           if (NH >= 2) bufH[(j0 + jj) * C::PSTR + pg] = f4(z, jj);
         }
-        __syncthreads();
+        cta_sync();
 #pragma unroll 1
         for (int k = NH; k >= 2; --k) {
           // dW^k, db^k
@@ -500,12 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           gemm_bwd<N, NH, DO>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
           st.load(k - 2, z);
           const float s = sSl[k - 2];
-          float sb = 0.0f;
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, sb));
-#pragma unroll
-          for (int kk = 0; kk < NH; ++kk)
-            if (kk == k - 2) sbar[kk] += sb;
+          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2));
           const bool more = (k - 1 >= 2);
           if (more) {
             st.load(k - 3, z);
@@ -513,13 +513,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 #pragma unroll
             for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2));
           }
-          __syncthreads();
+          cta_sync();
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
             bufZ[(j0 + jj) * C::PSTR + pg] = f4(hb, jj);
             if (more) bufH[(j0 + jj) * C::PSTR + pg] = f4(z, jj);
           }
-          __syncthreads();
+          cta_sync();
         }
         // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
         for (int j = tid; j < N; j += kThreads) {
@@ -535,35 +535,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           rmw_store(Pc + LY::offW(1) + 2 * j + 1, a1, first);
           rmw_store(Pc + LY::offB(1) + j, ab, first);
         }
-        // slopes (da^k = n dJ/ds_k) and loss partials
-        float red[NH + 4];
+        // loss partials; the slope entries of the partial stay 0 (K5 fills them)
+        float red[4];
 #pragma unroll
-        for (int k = 0; k < NH; ++k) red[k] = a.slope_n * sbar[k];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) red[NH + r] = lsum[r];
-        block_sum<NH + 4>(red, sRed);
+        for (int r = 0; r < 4; ++r) red[r] = lsum[r];
+        block_sum<4>(red, sRed);
         if (tid == 0) {
 #pragma unroll
-          for (int k = 0; k < NH; ++k) rmw_store(Pc + LY::offA(k + 1), red[k], first);
+          for (int r = 0; r < 4; ++r) rmw_store(a.partial_loss + size_t(c) * 4 + r, red[r], first);
+          if (first) {
 #pragma unroll
-          for (int r = 0; r < 4; ++r) rmw_store(a.partial_loss + size_t(c) * 4 + r, red[NH + r], first);
+            for (int k = 1; k <= NH; ++k) Pc[LY::offA(k)] = 0.0f;
+          }
         }
       }
     }
   }
   if constexpr (MODE == 0) {
     if (a.gstash == nullptr) {
-      __syncthreads();
+      cta_sync();
       tmem_fence_after();
-      if (tid < 32) tmem_dealloc512(*tslot);
+      if (tid < 32) {
+        __syncwarp();
+        tmem_dealloc512(*tslot);
+      }
     }
   }
 }
 
 // ----------------------------------------------------------------------------
-// K5: gradient reduction over chunk partials (fixed order), J assembly, Adam.
-// mode 0: reduce only; 1: reduce + Adam; 2: Adam on the stored gradient.
+// K5a k_reduce: gradient reduction over chunk partials (fixed order) and J_q
+// assembly (Eq. 5/6).  K5b k_slope_adam: slope gradients from the exact
+// homogeneity identity  a_k dJ/da_k = <W^k, dJ/dW^k> + <b^k, dJ/db^k>
+// (J depends on s_k = n a_k, W^k, b^k only through s_k W^k and s_k b^k),
+// evaluated as fp64 dot products, then optionally the Adam step.
 // ----------------------------------------------------------------------------
+constexpr int kMaxHidden = 8;
+constexpr int kRB = 256;
+
 struct RArgs {
   const float* partial;
   const float* partial_loss;
@@ -579,37 +588,22 @@ struct RArgs {
   const float4* sub_adam;     // lr, beta1, beta2, eps
   float* loss;                // [n_sub][8]
   int32_t* flag;              // non-finite flag
-  int mode;
+  int mode;                   // k_slope_adam: 0 slopes only, 1 slopes + Adam
+  int n_hidden;               // 0: skip the slope pass
+  int offW[kMaxHidden], nW[kMaxHidden], offB[kMaxHidden], nB[kMaxHidden], offA[kMaxHidden];
 };
 
-__global__ void k_reduce_adam(const RArgs r) {
+__global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
   const int q = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int c0 = r.sub_chunk[q], c1 = r.sub_chunk[q + 1];
-  const int t = r.tstep[q] + 1;
   if (i < r.pstride) {
-    float g;
-    if (r.mode == 2) {
-      g = r.grad[size_t(q) * r.pstride + i];
-    } else {
-      g = 0.0f;
-      for (int c = c0; c < c1; ++c) g += r.partial[size_t(c) * r.pstride + i];
-      r.grad[size_t(q) * r.pstride + i] = g;
-    }
+    float g = 0.0f;
+    for (int c = c0; c < c1; ++c) g += r.partial[size_t(c) * r.pstride + i];
+    r.grad[size_t(q) * r.pstride + i] = g;
     if (!isfinite(g)) atomicOr(r.flag, 2);
-    if (r.mode != 0) {
-      const float4 ad = r.sub_adam[q];
-      const size_t k = size_t(q) * r.pstride + i;
-      const float mm = ad.y * r.m[k] + (1.0f - ad.y) * g;
-      const float vv = ad.z * r.v[k] + (1.0f - ad.z) * g * g;
-      r.m[k] = mm;
-      r.v[k] = vv;
-      const float mh = mm / (1.0f - powf(ad.y, float(t)));
-      const float vh = vv / (1.0f - powf(ad.z, float(t)));
-      r.params[k] -= ad.x * mh / (sqrtf(vh) + ad.w);
-    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && r.mode != 2) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     float l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     for (int c = c0; c < c1; ++c)
       for (int e = 0; e < 4; ++e) l[e] += r.partial_loss[size_t(c) * 4 + e];
@@ -621,17 +615,58 @@ __global__ void k_reduce_adam(const RArgs r) {
     L[6] = 0.0f; L[7] = 0.0f;
     if (!isfinite(J)) atomicOr(r.flag, 1);
   }
-  if (r.mode != 0) {
-    // the last block of subdomain q advances its Adam step counter
+}
+
+__global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
+  __shared__ double red[kRB / 32];
+  const int q = blockIdx.y;
+  const int i0 = blockIdx.x * kRB;
+  const int tid = threadIdx.x;
+  const float* P = r.params + size_t(q) * r.pstride;
+  float* G = r.grad + size_t(q) * r.pstride;
+  for (int k = 0; k < r.n_hidden; ++k) {
+    const int oa = r.offA[k];
+    if (oa < i0 || oa >= i0 + kRB) continue;   // block-uniform
+    double acc = 0.0;
+    for (int e = tid; e < r.nW[k]; e += kRB) acc += double(P[r.offW[k] + e]) * double(G[r.offW[k] + e]);
+    for (int e = tid; e < r.nB[k]; e += kRB) acc += double(P[r.offB[k] + e]) * double(G[r.offB[k] + e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kRB / 32; ++w) s += red[w];
+      const float ga = float(s / double(P[oa]));
+      G[oa] = ga;
+      if (!isfinite(ga)) atomicOr(r.flag, 4);
+    }
+    __syncthreads();
+  }
+  if (r.mode == 0) return;
+  const int i = i0 + tid;
+  const int t = r.tstep[q] + 1;
+  if (i < r.pstride) {
+    const float g = G[i];
+    const float4 ad = r.sub_adam[q];
+    const size_t k = size_t(q) * r.pstride + i;
+    const float mm = ad.y * r.m[k] + (1.0f - ad.y) * g;
+    const float vv = ad.z * r.v[k] + (1.0f - ad.z) * g * g;
+    r.m[k] = mm;
+    r.v[k] = vv;
+    const float mh = mm / (1.0f - powf(ad.y, float(t)));
+    const float vh = vv / (1.0f - powf(ad.z, float(t)));
+    r.params[k] -= ad.x * mh / (sqrtf(vh) + ad.w);
+  }
+  // the last block of subdomain q advances its Adam step counter
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int prev = atomicAdd(&r.done[q], 1);
+    if (prev == int(gridDim.x) - 1) {
+      r.tstep[q] = t;
+      r.done[q] = 0;
       __threadfence();
-      const int prev = atomicAdd(&r.done[q], 1);
-      if (prev == int(gridDim.x) - 1) {
-        r.tstep[q] = t;
-        r.done[q] = 0;
-        __threadfence();
-      }
     }
   }
 }

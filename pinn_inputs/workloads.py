@@ -312,11 +312,12 @@ def build_problem(*, name: str, pde: str, method: str, nx: int, ny: int,
         subs.append(Subdomain(q, ix, iy, lo, hi, _f32(x_f), _f32(x_u), _f32(u_t), _f32(u_m),
                               my_edges, xavier_params(sizes, slope_n, wrng)))
 
+    f = lambda v: float(np.float32(v))    # scalar inputs are float32-exact too
     return Problem(name=name, method=method, pde=pde, activation=activation, d_in=2,
-                   d_out=d_out, width=width, n_hidden=n_hidden, slope_n=float(slope_n),
-                   nu=float(nu), re=float(re), w_u=float(weights[0]), w_f=float(weights[1]),
-                   w_i=float(weights[2]), w_if=float(weights[3]), lr=float(lr),
-                   beta1=float(betas[0]), beta2=float(betas[1]), eps=float(eps),
+                   d_out=d_out, width=width, n_hidden=n_hidden, slope_n=f(slope_n),
+                   nu=f(nu), re=f(re), w_u=f(weights[0]), w_f=f(weights[1]),
+                   w_i=f(weights[2]), w_if=f(weights[3]), lr=f(lr),
+                   beta1=f(betas[0]), beta2=f(betas[1]), eps=f(eps),
                    nx=nx, ny=ny, domain_lo=dlo, domain_hi=dhi, subdomains=subs, edges=edges)
 
 

@@ -159,6 +159,27 @@ def test_gradient_matches_central_differences(cfg, method):
     assert err < 1e-6, err
 
 
+@pytest.mark.parametrize("cfg,method", [("C1", "cpinn"), ("C2", "xpinn"), ("C4", "cpinn")])
+def test_slope_gradient_homogeneity_identity(cfg, method):
+    """J depends on (a^k, W^k, b^k) only through (n a^k W^k, n a^k b^k) (Eq. 2 with
+    the slope inside Phi), hence a^k dJ/da^k = <W^k, dJ/dW^k> + <b^k, dJ/db^k>
+    exactly, for every hidden layer k."""
+    from pinn_inputs import param_layout
+    kw = dict(n_f=30, n_i=6, n_u=8, width=6, n_hidden=3)
+    p = perturb_params(make_config(cfg, method=method, **kw), scale=0.3)
+    th = [torch.tensor(s.params) for s in p.subdomains]
+    q = p.n_sub - 1
+    _, g = OL.loss_and_grad(p, q, th)
+    t = th[q].numpy(); g = g.numpy()
+    for ent in param_layout(p.sizes):
+        if "a" not in ent:
+            continue
+        (ow, nw), (ob, nb), (oa, _) = ent["W"], ent["b"], ent["a"]
+        lhs = t[oa] * g[oa]
+        rhs = t[ow:ow + nw] @ g[ow:ow + nw] + t[ob:ob + nb] @ g[ob:ob + nb]
+        assert abs(lhs - rhs) <= 1e-10 * max(1.0, abs(rhs)), (lhs, rhs)
+
+
 def test_gradient_linearity():
     """grad(a L1 + b L2) = a grad L1 + b grad L2 (weights enter linearly)."""
     p = _small("C2", method="xpinn")
