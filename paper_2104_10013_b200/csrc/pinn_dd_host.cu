@@ -383,25 +383,38 @@ pinn_dd_status launch_k5(pinn_dd* h, int mode) {
   return PINN_DD_OK;
 }
 
-pinn_dd_status one_iteration(pinn_dd* h, bool timed) {
+// record = event timestamps around K2 / K1 / K5 (as external event-record
+// nodes when captured into the step graph)
+pinn_dd_status record(pinn_dd* h, int i, bool capturing) {
+  if (capturing)
+    CK(h, cudaEventRecordWithFlags(h->ev[i], h->stream, cudaEventRecordExternal));
+  else
+    CK(h, cudaEventRecord(h->ev[i], h->stream));
+  return PINN_DD_OK;
+}
+
+pinn_dd_status accumulate_times(pinn_dd* h) {
+  CK(h, cudaEventSynchronize(h->ev[3]));
+  float a = 0, b = 0, c = 0;
+  CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+  CK(h, cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
+  CK(h, cudaEventElapsedTime(&c, h->ev[2], h->ev[3]));
+  h->ms[0] += a;
+  h->ms[1] += b;
+  h->ms[2] += c;
+  return PINN_DD_OK;
+}
+
+pinn_dd_status one_iteration(pinn_dd* h, bool timed, bool capturing) {
   pinn_dd_status s;
-  if (timed) CK(h, cudaEventRecord(h->ev[0], h->stream));
+  if (timed && (s = record(h, 0, capturing)) != PINN_DD_OK) return s;
   if ((s = launch_k2(h)) != PINN_DD_OK) return s;
-  if (timed) CK(h, cudaEventRecord(h->ev[1], h->stream));
+  if (timed && (s = record(h, 1, capturing)) != PINN_DD_OK) return s;
   if ((s = launch_k1(h)) != PINN_DD_OK) return s;
-  if (timed) CK(h, cudaEventRecord(h->ev[2], h->stream));
+  if (timed && (s = record(h, 2, capturing)) != PINN_DD_OK) return s;
   if ((s = launch_k5(h, 1)) != PINN_DD_OK) return s;
-  if (timed) {
-    CK(h, cudaEventRecord(h->ev[3], h->stream));
-    CK(h, cudaEventSynchronize(h->ev[3]));
-    float a = 0, b = 0, c = 0;
-    cudaEventElapsedTime(&a, h->ev[0], h->ev[1]);
-    cudaEventElapsedTime(&b, h->ev[1], h->ev[2]);
-    cudaEventElapsedTime(&c, h->ev[2], h->ev[3]);
-    h->ms[0] += a;
-    h->ms[1] += b;
-    h->ms[2] += c;
-  }
+  if (timed && (s = record(h, 3, capturing)) != PINN_DD_OK) return s;
+  if (timed && !capturing) return accumulate_times(h);
   return PINN_DD_OK;
 }
 
@@ -640,7 +653,7 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
                 (long long)h->d.n_recv);
   if (n_iters < 0) return fail(h, PINN_DD_EINVAL, "n_iters < 0");
   const bool timed = (h->d.flags & PINN_DD_FLAG_TIMING) != 0;
-  const bool graph = (h->d.flags & PINN_DD_FLAG_GRAPH) != 0 && !timed;
+  const bool graph = (h->d.flags & PINN_DD_FLAG_GRAPH) != 0;
   pinn_dd_status s;
   for (int it = 0; it < n_iters; ++it) {
     if (graph) {
@@ -654,7 +667,7 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
           h->stream = user;
           return fail(h, PINN_DD_ECUDA, "graph capture: %s", cudaGetErrorString(e0));
         }
-        pinn_dd_status cs = one_iteration(h, false);
+        pinn_dd_status cs = one_iteration(h, timed, true);
         cudaError_t e = cudaStreamEndCapture(h->stream, &g);
         h->stream = user;
         if (cs != PINN_DD_OK) return cs;
@@ -669,7 +682,8 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
       CK(h, cudaEventRecord(h->gjoin[1], h->gstream));
       CK(h, cudaStreamWaitEvent(h->stream, h->gjoin[1], 0));
       h->launches += (h->n_chunks2 > 0 ? 4 : 3);
-    } else if ((s = one_iteration(h, timed)) != PINN_DD_OK) {
+      if (timed && (s = accumulate_times(h)) != PINN_DD_OK) return s;
+    } else if ((s = one_iteration(h, timed, false)) != PINN_DD_OK) {
       return s;
     }
   }

@@ -331,9 +331,12 @@ def _c1(scale, method=None, **kw):
                 n_f=500, n_i=50, n_u=100, width=20, n_hidden=3, lr=8e-4, seed_index=0)
 
 
-def _c2(scale, method=None, **kw):
-    return dict(name="C2-poisson-4x4-6x40", pde=kw.get("pde", "poisson"),
-                method=method or "cpinn", nx=4, ny=4, domain_lo=(0.0, 0.0), domain_hi=(1.0, 1.0),
+def _c2(scale, method=None, weak=1, **kw):
+    """C2 on [0,1]^2 (4x4); `weak` = G replicates the 4x4 block along x on
+    [0, G] x [0, 1] (4G x 4 subdomains, one 4x4 block per GPU: weak scaling)."""
+    return dict(name=f"C2-poisson-{4 * weak}x4-6x40", pde=kw.get("pde", "poisson"),
+                method=method or "cpinn", nx=4 * weak, ny=4, domain_lo=(0.0, 0.0),
+                domain_hi=(float(weak), 1.0),
                 n_f=15000, n_i=250, n_u=80, width=40, n_hidden=6, lr=6e-4, seed_index=1)
 
 
