@@ -18,10 +18,11 @@
 
 namespace pinn {
 
-constexpr int kThreads = 128;   // 4 warps = the 4 TMEM lane quarters
+constexpr int kThreads = 256;   // 8 warps: 2 per scheduler; warps w, w+4 share TMEM lane quarter w%4
 constexpr int kC = 4;           // jet channels
-constexpr int kJT = 20;         // neurons per thread (mapping A)
+constexpr int kJT = 10;         // neurons per thread (mapping A)
 constexpr int kA = kC * kJT;    // stash floats per thread per hidden layer
+constexpr int kStashCols = 256; // TMEM columns per thread (512 / 2 warps per lane quarter)
 
 __host__ __device__ constexpr int al4(int x) { return (x + 3) & ~3; }
 
@@ -68,8 +69,9 @@ constexpr bool lay_ok() {
 // Kernel geometry for width N (mapping A: thread = (point group pg, neuron block nb)).
 template <int N, int NH, int DO>
 struct KCfg {
-  static_assert(N % kJT == 0, "width must be a multiple of 20");
+  static_assert(N % kJT == 0, "width must be a multiple of kJT");
   static_assert(lay_ok<N, NH, DO>(), "closed-form parameter layout mismatch");
+  static_assert(NH * kA <= kStashCols, "reverse-mode stash exceeds the TMEM columns per thread");
   static constexpr int NB = N / kJT;           // neuron blocks
   static constexpr int P = kThreads / NB;      // points per tile (1 point per thread)
   static constexpr int PSTR = P + 1;           // float4 row stride of activation buffers (odd)
@@ -78,11 +80,13 @@ struct KCfg {
   static constexpr int WROWS = N * WS + NB * 4;            // floats per hidden W in smem
   // mapping B (dW): JB x IB register block, interleaved rows, S point splits
   static constexpr int JB = (N >= 80) ? 8 : 4;
-  static constexpr int IB = JB;
+  static constexpr int IB = 4;
   static constexpr int NJ = N / JB;
   static constexpr int NI = N / IB;
   static constexpr int NBLK = NJ * NI;
-  static constexpr int S = (kThreads / NBLK) >= 4 ? 4 : ((kThreads / NBLK) >= 2 ? 2 : 1);
+  static constexpr int S_MAX = kThreads / NBLK;
+  static constexpr int S = S_MAX >= 8 ? 8 : (S_MAX >= 4 ? 4 : (S_MAX >= 2 ? 2 : 1));
+  static_assert(P % S == 0, "points per split");
   // smem carve (in floats)
   static constexpr int oW1 = 0;                            // [N][2]
   static constexpr int oB1 = oW1 + 2 * N;                  // [N]
@@ -95,11 +99,13 @@ struct KCfg {
   static constexpr int BUF = N * PSTR * 4;
   static constexpr int oU = oBuf + 2 * BUF;                // [P][DO] float4
   static constexpr int oX = oU + P * DO * 4;               // [2][P]
-  static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [4 warps][4]
-  static constexpr int oDw = oRed + 16;                    // dW split scratch [S][NBLK][JB*IB] (S>1)
+  static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [8 warps][4]
+  static constexpr int oDw = oRed + 32;                    // dW split scratch [S][NBLK][JB*IB] (S>1)
   static constexpr int DWS = (S > 1) ? S * NBLK * JB * IB : 0;
   static constexpr int TOTAL = al4(oDw + DWS + 4);         // + tmem address slot
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(NBLK * S <= kThreads, "dW blocks per CTA");
 };
 
 // ----------------------------------------------------------------------------
@@ -124,34 +130,57 @@ __device__ __forceinline__ void act_derivs(float u, float& s0, float& s1, float&
   }
 }
 
-// forward jet map of one neuron: (z, g1, g2, L) -> (h_v, h_1, h_2, h_L)
+// What the reverse sweep needs of a hidden pre-activation jet (z, g1, g2, L):
+// sigma^(k)(s z) for k = 0..3 and (g1, g2, L).  For tanh every sigma^(k) is a
+// polynomial in t = tanh(s z), so the stash keeps (t, g1, g2, L) and the
+// reverse pass evaluates no transcendental; sin / cos keep z itself.
+template <int ACT>
+__device__ __forceinline__ float stash_x(float zx, float s) {
+  return ACT == 0 ? tanhf(s * zx) : zx;
+}
+template <int ACT>
+__device__ __forceinline__ void derivs_from_stash(float x, float s, float& s0, float& s1, float& s2, float& s3) {
+  if (ACT == 0) {
+    const float t = x;
+    s0 = t;
+    s1 = 1.0f - t * t;
+    s2 = -2.0f * t * s1;
+    s3 = s1 * (6.0f * t * t - 2.0f);
+  } else {
+    act_derivs<ACT>(s * x, s0, s1, s2, s3);
+  }
+}
+
+// forward jet map of one neuron from its stash form (x, g1, g2, L):
+// h = (sigma, sigma' s g1, sigma' s g2, sigma'' s^2 Q + sigma' s L)
 template <int ACT>
 __device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2) {
   float s0, s1, s2, s3;
-  act_derivs<ACT>(s * z.x, s0, s1, s2, s3);
-  float Q = m1 * z.y * z.y + m2 * z.z * z.z;
+  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3);
+  const float Q = m1 * z.y * z.y + m2 * z.z * z.z;
+  const float ss = s1 * s;
   float4 h;
   h.x = s0;
-  h.y = s1 * s * z.y;
-  h.z = s1 * s * z.z;
-  h.w = s2 * s * s * Q + s1 * s * z.w;
+  h.y = ss * z.y;
+  h.z = ss * z.z;
+  h.w = s2 * s * s * Q + ss * z.w;
   return h;
 }
 
-// adjoint of act_fwd: given hb = dJ/dh (4 channels) and the stashed z-jets,
-// return zb = dJ/dz (4 channels).  The slope gradient is NOT accumulated here:
-// J depends on (s_k, W^k, b^k) only through s_k W^k and s_k b^k, so
-// a_k dJ/da_k = <W^k, dJ/dW^k> + <b^k, dJ/db^k> exactly; K5 evaluates that
-// identity once per step.
+// adjoint of act_fwd: given hb = dJ/dh (4 channels) and the stash form of the
+// pre-activation jets, return zb = dJ/dz (4 channels).  The slope gradient is
+// NOT accumulated here: J depends on (s_k, W^k, b^k) only through s_k W^k and
+// s_k b^k, so a_k dJ/da_k = <W^k, dJ/dW^k> + <b^k, dJ/db^k> exactly; K5
+// evaluates that identity once per step.
 template <int ACT>
 __device__ __forceinline__ float4 act_bwd(float4 z, float4 hb, float s, float m1, float m2) {
   float s0, s1, s2, s3;
-  act_derivs<ACT>(s * z.x, s0, s1, s2, s3);
-  float Q = m1 * z.y * z.y + m2 * z.z * z.z;
-  float zb = hb.x * s1 + s * s2 * (hb.y * z.y + hb.z * z.z) + hb.w * (s3 * s * s * Q + s2 * s * z.w);
-  float g1 = hb.y * s1 + 2.0f * m1 * hb.w * s2 * s * z.y;
-  float g2 = hb.z * s1 + 2.0f * m2 * hb.w * s2 * s * z.z;
-  float lb = hb.w * s1;
+  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3);
+  const float Q = m1 * z.y * z.y + m2 * z.z * z.z;
+  const float zb = hb.x * s1 + s * s2 * (hb.y * z.y + hb.z * z.z) + hb.w * (s3 * s * s * Q + s2 * s * z.w);
+  const float g1 = hb.y * s1 + 2.0f * m1 * hb.w * s2 * s * z.y;
+  const float g2 = hb.z * s1 + 2.0f * m2 * hb.w * s2 * s * z.z;
+  const float lb = hb.w * s1;
   return make_float4(s * zb, s * g1, s * g2, s * lb);
 }
 
@@ -173,45 +202,40 @@ __device__ __forceinline__ void tmem_dealloc512(uint32_t taddr) {
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-      "%14, %15, %16};\n" ::"r"(taddr),
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
       "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
       "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15]))
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
-// load 16 columns and wait in the same asm block so the values are valid on exit
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
+// load 8 columns and wait in the same asm block so the values are valid on exit
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
       "tcgen05.wait::ld.sync.aligned;\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
       : "r"(taddr)
       : "memory");
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // Stash policy: TMEM (default) or a per-CTA global scratch (debug fallback).
+// Thread tid owns TMEM lane 32*(warp%4) + lane, columns [256*(warp/4), +256).
 struct Stash {
-  uint32_t taddr;     // TMEM base of this thread's lane quarter
+  uint32_t taddr;     // TMEM address of this thread's column block
   float* g;           // global fallback base for this CTA (or nullptr)
   int tid;
   __device__ __forceinline__ void store(int slot, const float* v) {
     if (g == nullptr) {
       __syncwarp();   // tcgen05.st is .sync.aligned: the warp must be converged
 #pragma unroll
-      for (int q = 0; q < kA / 16; ++q) tmem_st16(taddr + slot * kA + q * 16, v + q * 16);
+      for (int q = 0; q < kA / 8; ++q) tmem_st8(taddr + slot * kA + q * 8, v + q * 8);
       tmem_wait_st();
     } else {
 #pragma unroll
@@ -222,7 +246,7 @@ struct Stash {
     if (g == nullptr) {
       __syncwarp();   // tcgen05.ld is .sync.aligned
 #pragma unroll
-      for (int q = 0; q < kA / 16; ++q) tmem_ld16(taddr + slot * kA + q * 16, v + q * 16);
+      for (int q = 0; q < kA / 8; ++q) tmem_ld8(taddr + slot * kA + q * 8, v + q * 8);
     } else {
 #pragma unroll
       for (int a = 0; a < kA; ++a) v[a] = g[(size_t(slot) * kA + a) * kThreads + tid];

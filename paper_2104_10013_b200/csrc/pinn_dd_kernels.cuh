@@ -126,12 +126,12 @@ __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const fl
     const float4 zb = Zb[j * C::PSTR + pg];
     const float* wr = W + j * C::WS + (j / kJT) * 4 + j0;
 #pragma unroll
-    for (int q = 0; q < kJT / 4; ++q) {
-      const float4 w = *reinterpret_cast<const float4*>(wr + 4 * q);
-      const float ws[4] = {w.x, w.y, w.z, w.w};
+    for (int q = 0; q < kJT / 2; ++q) {
+      const float2 w = *reinterpret_cast<const float2*>(wr + 2 * q);
+      const float ws[2] = {w.x, w.y};
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int ii = 4 * q + m;
+      for (int m = 0; m < 2; ++m) {
+        const int ii = 2 * q + m;
         hb[ii] = fmaf(zb.x, ws[m], hb[ii]);
         hb[kJT + ii] = fmaf(zb.y, ws[m], hb[kJT + ii]);
         hb[2 * kJT + ii] = fmaf(zb.z, ws[m], hb[2 * kJT + ii]);
@@ -158,7 +158,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
     for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = 0.0f;
-#pragma unroll 1
+#pragma unroll 2
     for (int p = s * PS; p < (s + 1) * PS; ++p) {
       float4 zr[JB], hr[IB];
 #pragma unroll
@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       tmem_fence_before();
       cta_sync();
       tmem_fence_after();
-      st.taddr = *tslot + (uint32_t((tid >> 5) * 32) << 16);
+      const int warp = tid >> 5;
+      st.taddr = *tslot + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * kStashCols);
     } else {
       st.g = a.gstash + size_t(blockIdx.x) * NH * kA * kThreads;
     }
@@ -304,8 +305,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           z[2 * kJT + jj] = w1;                       // dz/dx2 = W^1[:,1]
           z[3 * kJT + jj] = 0.0f;                     // Delta z = 0
         }
-        if constexpr (MODE == 0) st.store(0, z);
         const float s = sSl[0];
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s);
+        if constexpr (MODE == 0) st.store(0, z);
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
       }
@@ -315,8 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         const float4* Hin = (k & 1) ? buf1 : buf0;
         float4* Hout = (k & 1) ? buf0 : buf1;
         gemm_fwd<N, NH, DO>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
-        if constexpr (MODE == 0) st.store(k - 1, z);
         const float s = sSl[k - 1];
+#pragma unroll
+        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s);
+        if constexpr (MODE == 0) st.store(k - 1, z);
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
         cta_sync();
