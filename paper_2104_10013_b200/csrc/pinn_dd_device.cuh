@@ -100,9 +100,12 @@ struct KCfg {
   static constexpr int oU = oBuf + 2 * BUF;                // [P][DO] float4
   static constexpr int oX = oU + P * DO * 4;               // [2][P]
   static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [8 warps][4]
-  static constexpr int oDw = oRed + 32;                    // dW split scratch [S][NBLK][JB*IB] (S>1)
-  static constexpr int DWS = (S > 1) ? S * NBLK * JB * IB : 0;
-  static constexpr int TOTAL = al4(oDw + DWS + 4);         // + tmem address slot
+  static constexpr int oDw = oRed + 32;                    // dW/db split scratch (S>1)
+  static constexpr int SCR = (S > 1) ? S * NBLK * JB * IB + S * NJ * JB : 0;
+  static constexpr int oAcc = al4(oDw + SCR);              // per-chunk gradient accumulator
+  static constexpr int ACC = Lay<N, NH, DO>::total();
+  static constexpr bool DW_SMEM = (size_t(al4(oAcc + ACC + 4)) * 4) <= 227 * 1024;
+  static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 4);   // + tmem address slot
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NBLK * S <= kThreads, "dW blocks per CTA");

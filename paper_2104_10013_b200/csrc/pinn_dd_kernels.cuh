@@ -79,8 +79,25 @@ __device__ __forceinline__ void load_weights(const float* G, float slope_n, floa
   for (int e = tid; e < NH; e += kThreads) sm[C::oSl + e] = slope_n * G[LY::offA(e + 1)];
 }
 
+// gradient accumulator: shared memory for the whole chunk (DWS), else the
+// chunk's global partial (read-modify-write per tile, `first` = first tile)
+template <bool DWS>
+__device__ __forceinline__ void acc_add(float* base, int off, float v, bool first) {
+  if constexpr (DWS) {
+    base[off] += v;
+  } else {
+    base[off] = first ? v : base[off] + v;
+  }
+}
+
+__device__ __forceinline__ float comp(const float4& v, int m) {
+  return m == 0 ? v.x : (m == 1 ? v.y : (m == 2 ? v.z : v.w));
+}
+
 // forward GEMM of one hidden layer for this thread's (point, neuron block):
-// z[c][jj] = sum_i W[j][i] Hin[i][p].c  (+ b on the value channel)
+// z[c][jj] = sum_i W[j][i] Hin[i][p].c  (+ b on the value channel).
+// Per i-quad all 4*kJT accumulators are updated once per input component, so
+// consecutive FMAs are independent.
 template <int N, int NH, int DO>
 __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const float* __restrict__ W,
                                          const float* __restrict__ b, float* z, int pg, int nb) {
@@ -96,19 +113,22 @@ __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const f
   const float* Wb = W + j0 * C::WS + nb * 4;
 #pragma unroll 2
   for (int i = 0; i < N; i += 4) {
-    const float4 h0 = Hin[(i + 0) * C::PSTR + pg];
-    const float4 h1 = Hin[(i + 1) * C::PSTR + pg];
-    const float4 h2 = Hin[(i + 2) * C::PSTR + pg];
-    const float4 h3 = Hin[(i + 3) * C::PSTR + pg];
+    float4 h[4];
 #pragma unroll
-    for (int jj = 0; jj < kJT; ++jj) {
-      const float4 w = *reinterpret_cast<const float4*>(Wb + jj * C::WS + i);
-      float a0 = z[jj], a1 = z[kJT + jj], a2 = z[2 * kJT + jj], a3 = z[3 * kJT + jj];
-      a0 = fmaf(w.x, h0.x, a0); a1 = fmaf(w.x, h0.y, a1); a2 = fmaf(w.x, h0.z, a2); a3 = fmaf(w.x, h0.w, a3);
-      a0 = fmaf(w.y, h1.x, a0); a1 = fmaf(w.y, h1.y, a1); a2 = fmaf(w.y, h1.z, a2); a3 = fmaf(w.y, h1.w, a3);
-      a0 = fmaf(w.z, h2.x, a0); a1 = fmaf(w.z, h2.y, a1); a2 = fmaf(w.z, h2.z, a2); a3 = fmaf(w.z, h2.w, a3);
-      a0 = fmaf(w.w, h3.x, a0); a1 = fmaf(w.w, h3.y, a1); a2 = fmaf(w.w, h3.z, a2); a3 = fmaf(w.w, h3.w, a3);
-      z[jj] = a0; z[kJT + jj] = a1; z[2 * kJT + jj] = a2; z[3 * kJT + jj] = a3;
+    for (int m = 0; m < 4; ++m) h[m] = Hin[(i + m) * C::PSTR + pg];
+    float4 w[kJT];
+#pragma unroll
+    for (int jj = 0; jj < kJT; ++jj) w[jj] = *reinterpret_cast<const float4*>(Wb + jj * C::WS + i);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+#pragma unroll
+      for (int jj = 0; jj < kJT; ++jj) {
+        const float wm = comp(w[jj], m);
+        z[jj] = fmaf(wm, h[m].x, z[jj]);
+        z[kJT + jj] = fmaf(wm, h[m].y, z[kJT + jj]);
+        z[2 * kJT + jj] = fmaf(wm, h[m].z, z[2 * kJT + jj]);
+        z[3 * kJT + jj] = fmaf(wm, h[m].w, z[3 * kJT + jj]);
+      }
     }
   }
 }
@@ -121,43 +141,54 @@ __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const fl
   const int j0 = nb * kJT;
 #pragma unroll
   for (int e = 0; e < kA; ++e) hb[e] = 0.0f;
-#pragma unroll 2
-  for (int j = 0; j < N; ++j) {
-    const float4 zb = Zb[j * C::PSTR + pg];
-    const float* wr = W + j * C::WS + (j / kJT) * 4 + j0;
+#pragma unroll 1
+  for (int jb = 0; jb < C::NB; ++jb) {
+    // rows jb*kJT .. +kJT-1 share the block skew jb*4
+    const float* Wrow = W + jb * (kJT * C::WS + 4) + j0;
+    const float4* Zrow = Zb + jb * kJT * C::PSTR + pg;
 #pragma unroll
-    for (int q = 0; q < kJT / 2; ++q) {
-      const float2 w = *reinterpret_cast<const float2*>(wr + 2 * q);
-      const float ws[2] = {w.x, w.y};
+    for (int jj = 0; jj < kJT; ++jj) {
+      const float4 zb = Zrow[jj * C::PSTR];
+      const float* wr = Wrow + jj * C::WS;
 #pragma unroll
-      for (int m = 0; m < 2; ++m) {
-        const int ii = 2 * q + m;
-        hb[ii] = fmaf(zb.x, ws[m], hb[ii]);
-        hb[kJT + ii] = fmaf(zb.y, ws[m], hb[kJT + ii]);
-        hb[2 * kJT + ii] = fmaf(zb.z, ws[m], hb[2 * kJT + ii]);
-        hb[3 * kJT + ii] = fmaf(zb.w, ws[m], hb[3 * kJT + ii]);
+      for (int q = 0; q < kJT / 2; ++q) {
+        const float2 w = *reinterpret_cast<const float2*>(wr + 2 * q);
+        const float ws[2] = {w.x, w.y};
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int ii = 2 * q + m;
+          hb[ii] = fmaf(zb.x, ws[m], hb[ii]);
+          hb[kJT + ii] = fmaf(zb.y, ws[m], hb[kJT + ii]);
+          hb[2 * kJT + ii] = fmaf(zb.z, ws[m], hb[2 * kJT + ii]);
+          hb[3 * kJT + ii] = fmaf(zb.w, ws[m], hb[3 * kJT + ii]);
+        }
       }
     }
   }
 }
 
-// weight gradient of one hidden layer (mapping B):
-// dW[j][i] += sum_p sum_c Zb[j][p].c H[i][p].c, rows/cols interleaved per thread.
-template <int N, int NH, int DO>
-__device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const float4* __restrict__ H, float* dst,
-                                        bool first, float* sDw) {
+// weight and bias gradient of one hidden layer (mapping B):
+// dW[j][i] += sum_p sum_c Zb[j][p].c H[i][p].c ;  db[j] += sum_p Zb[j][p].x
+// thread = (row block jb, column block ib, point split s); rows/cols interleaved.
+template <int N, int NH, int DO, bool DWS>
+__device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const float4* __restrict__ H, float* accW,
+                                        float* accB, bool first, float* sDw) {
   using C = KCfg<N, NH, DO>;
   constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
   constexpr int PS = C::P / S;
+  constexpr int DBOFF = S * NBLK * JB * IB;
   const int tid = threadIdx.x;
   if (tid < NBLK * S) {
     const int r = tid % NBLK, s = tid / NBLK;
     const int jb = r / NI, ib = r % NI;
     float acc[JB][IB];
+    float db[JB];
 #pragma unroll
-    for (int jj = 0; jj < JB; ++jj)
+    for (int jj = 0; jj < JB; ++jj) {
+      db[jj] = 0.0f;
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = 0.0f;
+    }
 #pragma unroll 2
     for (int p = s * PS; p < (s + 1) * PS; ++p) {
       float4 zr[JB], hr[IB];
@@ -166,35 +197,32 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) hr[ii] = H[(ib + NI * ii) * C::PSTR + p];
 #pragma unroll
-      for (int jj = 0; jj < JB; ++jj)
-#pragma unroll
-        for (int ii = 0; ii < IB; ++ii) {
-          float a = acc[jj][ii];
-          a = fmaf(zr[jj].x, hr[ii].x, a);
-          a = fmaf(zr[jj].y, hr[ii].y, a);
-          a = fmaf(zr[jj].z, hr[ii].z, a);
-          a = fmaf(zr[jj].w, hr[ii].w, a);
-          acc[jj][ii] = a;
-        }
-    }
-    if constexpr (S == 1) {
-      float old[JB][IB];
-      if (!first) {
+      for (int m = 0; m < 4; ++m)
 #pragma unroll
         for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
-          for (int ii = 0; ii < IB; ++ii) old[jj][ii] = dst[(jb + NJ * jj) * N + ib + NI * ii];
-      }
+          for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = fmaf(comp(zr[jj], m), comp(hr[ii], m), acc[jj][ii]);
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj) db[jj] += zr[jj].x;
+    }
+    if constexpr (S == 1) {
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
-        for (int ii = 0; ii < IB; ++ii)
-          dst[(jb + NJ * jj) * N + ib + NI * ii] = first ? acc[jj][ii] : old[jj][ii] + acc[jj][ii];
+        for (int ii = 0; ii < IB; ++ii) acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, acc[jj][ii], first);
+      if (ib == 0) {
+#pragma unroll
+        for (int jj = 0; jj < JB; ++jj) acc_add<DWS>(accB, jb + NJ * jj, db[jj], first);
+      }
     } else {
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
         for (int ii = 0; ii < IB; ++ii) sDw[(s * NBLK + r) * JB * IB + jj * IB + ii] = acc[jj][ii];
+      if (ib == 0) {
+#pragma unroll
+        for (int jj = 0; jj < JB; ++jj) sDw[DBOFF + (s * NJ + jb) * JB + jj] = db[jj];
+      }
     }
   }
   if constexpr (S > 1) {
@@ -205,7 +233,14 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int s = 0; s < S; ++s) v += sDw[(s * NBLK + r) * JB * IB + jj * IB + ii];
       const int jb = r / NI, ib = r % NI;
-      rmw_store(dst + (jb + NJ * jj) * N + ib + NI * ii, v, first);
+      acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v, first);
+    }
+    for (int e = tid; e < NJ * JB; e += kThreads) {
+      const int jb = e / JB, jj = e % JB;
+      float v = 0.0f;
+#pragma unroll
+      for (int s = 0; s < S; ++s) v += sDw[DBOFF + (s * NJ + jb) * JB + jj];
+      acc_add<DWS>(accB, jb + NJ * jj, v, first);
     }
   }
 }
@@ -239,6 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
   float* sY = sX + C::P;
   float* sRed = sm + C::oRed;
   float* sDw = sm + C::oDw;
+  float* sAcc = sm + C::oAcc;
+  constexpr bool DSM = C::DW_SMEM;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::TOTAL - 4);
   const float m1 = a.m1, m2 = a.m2;
   constexpr int NF = DO + (DO == 3 ? 3 : 1);
@@ -274,6 +311,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
     }
     const float4 lw = a.sub_w[ch.sub];
     float* Pc = a.partial + size_t(c) * a.pstride;
+    float* A = DSM ? sAcc : Pc;   // gradient accumulator of this chunk
+    if constexpr (MODE == 0 && DSM) {
+      cta_sync();
+      for (int e = tid; e < C::ACC; e += kThreads) sAcc[e] = 0.0f;
+    }
     const int ntiles = (ch.count + C::P - 1) / C::P;
 #pragma unroll 1
     for (int t = 0; t < ntiles; ++t) {
@@ -452,12 +494,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
             const float4 ub = sU[p * DO + o];
             acc = fmaf(h.x, ub.x, fmaf(h.y, ub.y, fmaf(h.z, ub.z, fmaf(h.w, ub.w, acc))));
           }
-          rmw_store(Pc + LY::offW(NH + 1) + idx, acc, first);
+          acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
         }
         if (tid < DO) {
           float acc = 0.0f;
           for (int p = 0; p < C::P; ++p) acc += sU[p * DO + tid].x;
-          rmw_store(Pc + LY::offB(NH + 1) + tid, acc, first);
+          acc_add<DSM>(A, LY::offB(NH + 1) + tid, acc, first);
         }
         float hb[kA];
 #pragma unroll
@@ -498,13 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 #pragma unroll 1
         for (int k = NH; k >= 2; --k) {
           // dW^k, db^k
-          gemm_dw<N, NH, DO>(bufZ, bufH, Pc + LY::offW(k), first, sDw);
-          for (int j = tid; j < N; j += kThreads) {
-            float acc = 0.0f;
-#pragma unroll 4
-            for (int p = 0; p < C::P; ++p) acc += bufZ[j * C::PSTR + p].x;
-            rmw_store(Pc + LY::offB(k) + j, acc, first);
-          }
+          gemm_dw<N, NH, DO, DSM>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);
           // adjoint of H^{k-1}, then of Z^{k-1}
           gemm_bwd<N, NH, DO>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
           st.load(k - 2, z);
@@ -536,9 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
             a1 = fmaf(zb.x, sY[p], a1) + zb.z;
             ab += zb.x;
           }
-          rmw_store(Pc + LY::offW(1) + 2 * j, a0, first);
-          rmw_store(Pc + LY::offW(1) + 2 * j + 1, a1, first);
-          rmw_store(Pc + LY::offB(1) + j, ab, first);
+          acc_add<DSM>(A, LY::offW(1) + 2 * j, a0, first);
+          acc_add<DSM>(A, LY::offW(1) + 2 * j + 1, a1, first);
+          acc_add<DSM>(A, LY::offB(1) + j, ab, first);
         }
         // loss partials; the slope entries of the partial stay 0 (K5 fills them)
         float red[4];
@@ -548,12 +584,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         if (tid == 0) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) rmw_store(a.partial_loss + size_t(c) * 4 + r, red[r], first);
-          if (first) {
+          if (first && !DSM) {
 #pragma unroll
             for (int k = 1; k <= NH; ++k) Pc[LY::offA(k)] = 0.0f;
           }
         }
       }
+    }
+    if constexpr (MODE == 0 && DSM) {
+      // flush the chunk's gradient (slope slots stay 0; K5 fills them)
+      cta_sync();
+      for (int e = tid; e < C::ACC; e += kThreads) Pc[e] = sAcc[e];
     }
   }
   if constexpr (MODE == 0) {
