@@ -254,15 +254,16 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize(dev)
     clocks.start()
+    time.sleep(0.5)                                        # let nvidia-smi start sampling
     for k in range(args.steps):
         flush.zero_()                                      # L2 flush, outside the events
         starts[k].record(stream)
         step()
         ends[k].record(stream)
     torch.cuda.synchronize(dev)
+    clk = clocks.stop()
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = sum(step_ms)
     kt = h.kernel_times()                                  # K2, K1, K5 ms over the timed steps, launches
@@ -348,8 +349,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--method", choices=["cpinn", "xpinn"], default="cpinn")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

@@ -55,24 +55,26 @@ __device__ __forceinline__ void block_sum(T* v, T* red) {
 }
 
 template <int N, int NH, int DO>
-__device__ __forceinline__ void load_weights(const float* G, float slope_n, float* sm) {
+__device__ __forceinline__ void load_weights(const float* __restrict__ G, float slope_n, float* sm) {
   using C = KCfg<N, NH, DO>;
   using LY = Lay<N, NH, DO>;
   const int tid = threadIdx.x;
-  for (int e = tid; e < 2 * N; e += kThreads) sm[C::oW1 + e] = G[LY::offW(1) + e];
-  for (int e = tid; e < N; e += kThreads) sm[C::oB1 + e] = G[LY::offB(1) + e];
+  for (int e = tid; e < 3 * N; e += kThreads) sm[C::oW1 + e] = G[LY::offW(1) + e];   // W^1 [N][2], b^1 (offB(1) = 2N)
+  static_assert(LY::offB(1) == 2 * N && C::oB1 == 2 * N, "W^1/b^1 contiguous");
+  // hidden W^k rows: float4 copies; row j of layer k lands at j*WS + (j/kJT)*4
+  constexpr int Q = N / 4;   // float4 per row
 #pragma unroll 1
   for (int k = 2; k <= NH; ++k) {
-    const float* W = G + LY::offW(k);
+    const float4* W = reinterpret_cast<const float4*>(G + LY::offW(k));
     float* dst = sm + C::oWh + (k - 2) * C::WROWS;
-    for (int e = tid; e < N * N; e += kThreads) {
-      const int j = e / N, i = e % N;
-      dst[j * C::WS + (j / kJT) * 4 + i] = W[e];
+    for (int e = tid; e < N * Q; e += kThreads) {
+      const int j = e / Q, q = e - (e / Q) * Q;
+      *reinterpret_cast<float4*>(dst + j * C::WS + (j / kJT) * 4 + 4 * q) = W[e];
     }
     for (int e = tid; e < N; e += kThreads) sm[C::oBh + (k - 2) * N + e] = G[LY::offB(k) + e];
   }
   for (int e = tid; e < DO * N; e += kThreads) {
-    const int o = e / N, i = e % N;
+    const int o = e / N, i = e - (e / N) * N;
     sm[C::oWo + o * C::WS + i] = G[LY::offW(NH + 1) + e];
   }
   for (int e = tid; e < DO; e += kThreads) sm[C::oBo + e] = G[LY::offB(NH + 1) + e];
@@ -300,9 +302,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
     }
   }
 
+  // contiguous chunk range per CTA: consecutive chunks mostly share a subdomain,
+  // so its weights are staged into shared memory once
+  const int c_beg = int((int64_t(a.n_chunks) * blockIdx.x) / gridDim.x);
+  const int c_end = int((int64_t(a.n_chunks) * (blockIdx.x + 1)) / gridDim.x);
   int cur_sub = -1;
 #pragma unroll 1
-  for (int c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+  for (int c = c_beg; c < c_end; ++c) {
     const Chunk ch = a.chunks[c];
     if (ch.sub != cur_sub) {
       cta_sync();
