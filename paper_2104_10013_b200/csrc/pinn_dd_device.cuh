@@ -79,13 +79,13 @@ struct KCfg {
   static constexpr int WS = al4(N);
   static constexpr int WROWS = N * WS + NB * 4;            // floats per hidden W in smem
   // mapping B (dW): JB x IB register block, interleaved rows, S point splits
-  static constexpr int JB = (N >= 80) ? 8 : 4;
-  static constexpr int IB = 4;
+  static constexpr int JB = 5;
+  static constexpr int IB = 5;
   static constexpr int NJ = N / JB;
   static constexpr int NI = N / IB;
   static constexpr int NBLK = NJ * NI;
   static constexpr int S_MAX = kThreads / NBLK;
-  static constexpr int S = S_MAX >= 8 ? 8 : (S_MAX >= 4 ? 4 : (S_MAX >= 2 ? 2 : 1));
+  static constexpr int S = S_MAX >= 16 ? 16 : (S_MAX >= 8 ? 8 : (S_MAX >= 4 ? 4 : (S_MAX >= 2 ? 2 : 1)));
   static_assert(P % S == 0, "points per split");
   // smem carve (in floats)
   static constexpr int oW1 = 0;                            // [N][2]
@@ -109,6 +109,7 @@ struct KCfg {
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NBLK * S <= kThreads, "dW blocks per CTA");
+
 };
 
 // ----------------------------------------------------------------------------

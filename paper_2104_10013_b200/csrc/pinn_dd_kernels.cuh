@@ -182,7 +182,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
   const int tid = threadIdx.x;
   if (tid < NBLK * S) {
     const int r = tid % NBLK, s = tid / NBLK;
-    const int jb = r / NI, ib = r % NI;
+    const int jb = r % NJ, ib = r / NJ;   // a warp covers 8 row blocks x 4 column blocks
     float acc[JB][IB];
     float db[JB];
 #pragma unroll
@@ -234,7 +234,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
       float v = 0.0f;
 #pragma unroll
       for (int s = 0; s < S; ++s) v += sDw[(s * NBLK + r) * JB * IB + jj * IB + ii];
-      const int jb = r / NI, ib = r % NI;
+      const int jb = r % NJ, ib = r / NJ;
       acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v, first);
     }
     for (int e = tid; e < NJ * JB; e += kThreads) {
@@ -491,16 +491,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 
         // ------------------------------------------------------------ reverse
         // output layer: dW^L, db^L
-        for (int idx = tid; idx < DO * N; idx += kThreads) {
+        for (int t4 = tid; t4 < 4 * DO * N; t4 += kThreads) {   // warp-uniform trip count
+          const int qq = t4 & 3, idx = t4 >> 2;
           const int o = idx / N, i = idx % N;
           float acc = 0.0f;
 #pragma unroll 4
-          for (int p = 0; p < C::P; ++p) {
+          for (int p = qq; p < C::P; p += 4) {
             const float4 h = HL[i * C::PSTR + p];
             const float4 ub = sU[p * DO + o];
             acc = fmaf(h.x, ub.x, fmaf(h.y, ub.y, fmaf(h.z, ub.z, fmaf(h.w, ub.w, acc))));
           }
-          acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
+          acc += __shfl_xor_sync(__activemask(), acc, 1);
+          acc += __shfl_xor_sync(__activemask(), acc, 2);
+          if (qq == 0) acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
         }
         if (tid < DO) {
           float acc = 0.0f;
@@ -569,18 +572,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           cta_sync();
         }
         // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
-        for (int j = tid; j < N; j += kThreads) {
+        for (int t4 = tid; t4 < 4 * N; t4 += kThreads) {
+          const int qq = t4 & 3, j = t4 >> 2;
           float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
 #pragma unroll 4
-          for (int p = 0; p < C::P; ++p) {
+          for (int p = qq; p < C::P; p += 4) {
             const float4 zb = bufZ[j * C::PSTR + p];
             a0 = fmaf(zb.x, sX[p], a0) + zb.y;
             a1 = fmaf(zb.x, sY[p], a1) + zb.z;
             ab += zb.x;
           }
-          acc_add<DSM>(A, LY::offW(1) + 2 * j, a0, first);
-          acc_add<DSM>(A, LY::offW(1) + 2 * j + 1, a1, first);
-          acc_add<DSM>(A, LY::offB(1) + j, ab, first);
+          const unsigned mk = __activemask();
+#pragma unroll
+          for (int o = 1; o < 4; o <<= 1) {
+            a0 += __shfl_xor_sync(mk, a0, o);
+            a1 += __shfl_xor_sync(mk, a1, o);
+            ab += __shfl_xor_sync(mk, ab, o);
+          }
+          if (qq == 0) {
+            acc_add<DSM>(A, LY::offW(1) + 2 * j, a0, first);
+            acc_add<DSM>(A, LY::offW(1) + 2 * j + 1, a1, first);
+            acc_add<DSM>(A, LY::offB(1) + j, ab, first);
+          }
         }
         // loss partials; the slope entries of the partial stay 0 (K5 fills them)
         float red[4];
