@@ -229,13 +229,16 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
   }
   if constexpr (S > 1) {
     cta_sync();
-    for (int e = tid; e < NBLK * JB * IB; e += kThreads) {
-      const int r = e / (JB * IB), jj = (e % (JB * IB)) / IB, ii = e % IB;
-      float v = 0.0f;
-#pragma unroll
-      for (int s = 0; s < S; ++s) v += sDw[(s * NBLK + r) * JB * IB + jj * IB + ii];
+    for (int e = tid; e < NBLK * JB; e += kThreads) {   // (block, row) items; IB columns each
+      const int r = e / JB, jj = e - (e / JB) * JB;
       const int jb = r % NJ, ib = r / NJ;
-      acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v, first);
+#pragma unroll
+      for (int ii = 0; ii < IB; ++ii) {
+        float v = 0.0f;
+#pragma unroll
+        for (int s = 0; s < S; ++s) v += sDw[(s * NBLK + r) * JB * IB + jj * IB + ii];
+        acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v, first);
+      }
     }
     for (int e = tid; e < NJ * JB; e += kThreads) {
       const int jb = e / JB, jj = e % JB;
