@@ -118,6 +118,39 @@ def subdomain_loss(prob, q: int, thetas: Sequence[torch.Tensor],
     return total, (mse_u, mse_f, mse_uavg, mse_if)
 
 
+def subdomain_loss_terms(prob, q: int, thetas: Sequence[torch.Tensor], chunk: int = 8192):
+    """The four MSE terms and J of subdomain q (same definitions as
+    `subdomain_loss`), evaluated in point chunks without a parameter graph, for
+    full-size problems.  Sums of squares are accumulated in float64."""
+    s = prob.subdomains[q]
+    th = thetas[q].detach()
+    sq = torch.zeros((), dtype=DT)
+    X_f = _t(s.x_f)
+    for i in range(0, len(X_f), chunk):
+        fl, Xg = eval_fields(prob, th, X_f[i:i + chunk], create_graph=False)
+        r = opde.residual(prob, fl, Xg).detach()
+        sq = sq + (r * r).sum()
+    mse_f = sq / len(X_f) if len(X_f) else torch.zeros((), dtype=DT)
+    with torch.no_grad():
+        if len(s.x_u):
+            u = onet.forward(th, prob.sizes, _t(s.x_u), prob.activation, prob.slope_n)
+            mse_u = _mse_sum(_t(s.u_mask) * (_t(s.u_target) - u))
+        else:
+            mse_u = torch.zeros((), dtype=DT)
+    mse_uavg = torch.zeros((), dtype=DT)
+    mse_if = torch.zeros((), dtype=DT)
+    for e in s.edges:
+        ed = prob.edges[e]
+        nb = prob.edge_neighbor(q, e)
+        X_i = _t(ed.pts)
+        u_q, s_q = interface_payload(prob, th, X_i, ed.normal, create_graph=False)
+        u_n, s_n = interface_payload(prob, thetas[nb].detach(), X_i, ed.normal, create_graph=False)
+        mse_uavg = mse_uavg + _mse_sum(u_q - 0.5 * (u_q + u_n))
+        mse_if = mse_if + _mse_sum(s_q - s_n)
+    total = prob.w_u * mse_u + prob.w_f * mse_f + prob.w_i * mse_uavg + prob.w_if * mse_if
+    return Breakdown(float(mse_u), float(mse_f), float(mse_uavg), float(mse_if), float(total))
+
+
 def loss_and_grad(prob, q: int, thetas: Sequence[torch.Tensor], payloads=None):
     th = thetas[q].detach().clone().requires_grad_(True)
     ths = list(thetas)

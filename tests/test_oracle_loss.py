@@ -235,3 +235,16 @@ def test_train_step_decreases_loss_on_average():
     for _ in range(29):
         st, bd = OL.train_step(p, st)
     assert sum(b.total for b in bd) < sum(b.total for b in bd0)
+
+
+@pytest.mark.parametrize("cfg,method", [("C2", "cpinn"), ("C4", "xpinn")])
+def test_chunked_loss_terms_match_graph_loss(cfg, method):
+    """The chunked, no-grad evaluation used for full-size checks equals the
+    graph-building Eq. (5)/(6) evaluation."""
+    p = perturb_params(_small(cfg, method=method, n_f=50), scale=0.2)
+    th = [torch.tensor(s.params) for s in p.subdomains]
+    for q in (0, p.n_sub - 1):
+        J, parts = OL.subdomain_loss(p, q, th)
+        bd = OL.subdomain_loss_terms(p, q, th, chunk=7)
+        ref = [float(x) for x in parts] + [float(J)]
+        np.testing.assert_allclose(bd.as_list(), ref, rtol=1e-12, atol=1e-15)

@@ -285,3 +285,43 @@ def test_full_size_c2_parity():
     for method in ("cpinn", "xpinn"):
         prob = make_config("C2", method=method)
         run_parity(prob, f"full C2 {method}")
+
+
+def test_full_size_c3_parity():
+    """BASELINE configs[2] at full size (4x2 x-t XPINN, 20000 residual points per
+    subdomain): loss terms and gradients vs the oracle."""
+    prob = make_config("C3", method="xpinn", gpus=8)
+    run_parity(prob, "full C3")
+
+
+def test_full_size_c4_sampled():
+    """BASELINE configs[3] at full size (8 x 125000 residual points, 5x80 NS):
+    every interface payload row, and the loss terms of two sampled subdomains
+    (chunked no-grad oracle); the chunk/tile structure is the one bench-style
+    full-size launches use."""
+    prob = make_config("C4", method="xpinn")
+    m = _handle(prob)
+    m.interface_payload()
+    loss, _ = m.loss_grad(want_grad=False)
+    torch.cuda.synchronize()
+    pay = m.payload.cpu().numpy()
+    th = OL.init_state(prob).thetas
+    ref = OL.all_payloads(prob, th)
+    t = m.table
+    for qi, q in enumerate(t.local):
+        pos = int(t.sub_off[qi] + t.n_res[qi] + t.n_data[qi])
+        for si in range(t.seg_off[qi], t.seg_off[qi + 1]):
+            e = int(t.seg_edge[si]); n = int(t.seg_n[si])
+            u, s = ref[(q, e)]
+            want = np.concatenate([u.numpy(), s.numpy()], axis=1)
+            got = pay[pos:pos + n, :want.shape[1]]
+            scale = np.max(np.abs(want), axis=0) + 1e-30
+            assert np.all(np.abs(got - want) <= 1e-4 * scale + 1e-7), (q, e)
+            pos += n
+    l = loss.cpu().numpy()
+    for q in (0, 5):
+        bd = OL.subdomain_loss_terms(prob, q, th).as_list()
+        J = abs(bd[4])
+        for i in range(5):
+            assert abs(l[q, i] - bd[i]) <= 1e-5 * abs(bd[i]) + 1e-6 * J, (q, i, l[q, i], bd[i])
+    m.close()
