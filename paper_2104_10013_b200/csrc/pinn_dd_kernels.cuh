@@ -191,7 +191,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = 0.0f;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (int p = s * PS; p < (s + 1) * PS; ++p) {
       float4 zr[JB], hr[IB];
 #pragma unroll
