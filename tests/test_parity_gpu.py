@@ -325,3 +325,50 @@ def test_full_size_c4_sampled():
         for i in range(5):
             assert abs(l[q, i] - bd[i]) <= 1e-5 * abs(bd[i]) + 1e-6 * J, (q, i, l[q, i], bd[i])
     m.close()
+
+
+def test_train_cpinn_poisson_to_accuracy():
+    """f4: 3000 graph-replayed Algorithm-1 iterations of a reduced C2 cPINN; the
+    Eq. (4) stitched prediction approaches u* = sin(pi x) sin(pi y) (Z15)."""
+    prob = make_config("C2", method="cpinn", n_f=2000, n_i=60, n_u=80, lr=2e-3)
+    m = _handle(prob)
+    g = np.linspace(0, 1, 41).astype(np.float32)
+    X = np.stack(np.meshgrid(g, g, indexing="ij"), -1).reshape(-1, 2)
+    own = OL.owners(prob, X.astype(np.float64))
+    owners = np.full((len(X), 4), -1, np.int32)
+    for i, o in enumerate(own):
+        owners[i, :len(o)] = o
+    pts = torch.tensor(X.T.copy(), device="cuda:0")
+    ow = torch.tensor(owners, device="cuda:0")
+    ref = np.sin(np.pi * X[:, 0]) * np.sin(np.pi * X[:, 1])
+    err0 = np.linalg.norm(m.predict(pts, ow).cpu().numpy()[0] - ref) / np.linalg.norm(ref)
+    m.step(3000, want_loss=False)
+    u = m.predict(pts, ow).cpu().numpy()[0]
+    err = np.linalg.norm(u - ref) / np.linalg.norm(ref)
+    assert err < 0.08 and err < 0.1 * err0, (err0, err)
+    assert m.adam_t(0) == 3000
+    m.close()
+
+
+def test_nonfinite_is_reported():
+    from paper_2104_10013_b200.binding import PinnDDError, ENONFINITE
+    prob = make_config("C1", n_f=100, n_i=10, n_u=20)
+    m = _handle(prob)
+    bad = m.get(0, 0).clone()
+    bad[3] = float("nan")
+    m.set(0, bad, 0)
+    with pytest.raises(PinnDDError) as ei:
+        m.step(1)
+    assert ei.value.status == ENONFINITE
+    m.close()
+
+
+def test_step_rejects_remote_twins():
+    from paper_2104_10013_b200.binding import PinnDD, PinnDDError, EPROTOCOL
+    prob = make_config("C2", method="xpinn", n_f=100, n_i=10, n_u=10)
+    owner = [0 if s.iy < 2 else 1 for s in prob.subdomains]
+    h = PinnDD(prob, [q for q in range(16) if owner[q] == 0], owner, 0, device="cuda:0")
+    with pytest.raises(PinnDDError) as ei:
+        h.step(1)
+    assert ei.value.status == EPROTOCOL
+    h.close()
