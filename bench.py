@@ -291,8 +291,7 @@ def run_ours(args):
         if world == 1:
             loss = h.step(1, want_loss=True)               # D2H of the loss breakdown (synchronises)
         else:
-            h.step_distributed(1, group)
-            loss = h.loss_grad(want_grad=False)[0].cpu()
+            loss = h.step_distributed(1, group, want_loss=True)   # D2H of the loss breakdown
     torch.cuda.synchronize(dev)
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if world > 1:

@@ -321,13 +321,19 @@ class PinnDD:
         self._check(self.lib.pinn_dd_step(self.h, int(n_iters), p))
         return out
 
-    def step_distributed(self, n_iters: int = 1, group=None):
-        """Algorithm 1 with remote neighbours: payload -> exchange -> loss+grad -> Adam."""
+    def step_distributed(self, n_iters: int = 1, group=None, want_loss: bool = False):
+        """Algorithm 1 with remote neighbours: payload (K2) ->
+        exchange with the neighbouring ranks -> loss + gradient (K1, K5a) -> Adam
+        (K5b).  Returns the last iteration's [n_sub, 8] loss breakdown (host) if
+        want_loss."""
+        if not hasattr(self, "_loss_dev"):
+            self._loss_dev = torch.empty(self.n_sub, 8, dtype=torch.float32, device=self.device)
         for _ in range(n_iters):
             self.interface_payload()
             exchange_payload(self.payload, self.table.plan, group)
-            self._check(self.lib.pinn_dd_loss_grad(self.h, None, None))
+            self._check(self.lib.pinn_dd_loss_grad(self.h, C.c_void_p(self._loss_dev.data_ptr()), None))
             self.adam()
+        return self._loss_dev.cpu().numpy() if want_loss else None
 
     def predict(self, pts: torch.Tensor, owners: torch.Tensor) -> torch.Tensor:
         """pts [2, n] float32, owners [n, 4] int32 local ids (-1 unused) -> [d_out, n]."""
@@ -378,9 +384,13 @@ def exchange_payload(payload: torch.Tensor, plan: ExchangePlan, group=None):
     if not plan.send and not plan.recv:
         return
     ops, bufs = [], []
+    cache = plan.__dict__.setdefault("_idx_cache", {})
     for peer in sorted(set(plan.send) | set(plan.recv)):
         if peer in plan.send:
-            idx = torch.as_tensor(plan.send[peer], device=payload.device)
+            key = (peer, str(payload.device))
+            if key not in cache:
+                cache[key] = torch.as_tensor(plan.send[peer], device=payload.device)
+            idx = cache[key]
             sbuf = payload.index_select(0, idx).contiguous()
             bufs.append(sbuf)
             ops.append(dist.P2POp(dist.isend, sbuf, peer, group))
