@@ -65,7 +65,10 @@ typedef enum {
   PINN_DD_EPROTOCOL = 6      /* interface segment without a twin, remote twin used by pinn_dd_step */
 } pinn_dd_status;
 
-enum { PINN_DD_METHOD_PINN = 0, PINN_DD_METHOD_CPINN = 1, PINN_DD_METHOD_XPINN = 2 };
+/* HYBRID ("cPINN in space + XPINN in time"): per interface edge, normal-flux
+   continuity on x1-normal edges (cPINN, Eq. 5) and residual continuity on
+   x2-normal edges (XPINN, Eq. 6). */
+enum { PINN_DD_METHOD_PINN = 0, PINN_DD_METHOD_CPINN = 1, PINN_DD_METHOD_XPINN = 2, PINN_DD_METHOD_HYBRID = 3 };
 /* P:313-316 Burgers; P:823-829 heat (K known; POISSON = K==1 with u* = sin(pi x) sin(pi y));
    P:415-417 steady incompressible NS (outputs u, v, p). */
 enum { PINN_DD_PDE_BURGERS = 0, PINN_DD_PDE_POISSON = 1, PINN_DD_PDE_HEAT = 2, PINN_DD_PDE_NS = 3 };

@@ -48,12 +48,24 @@ def eval_fields(prob, theta, X, create_graph=True):
     return fl, Xg
 
 
+def uses_flux(prob, normal) -> bool:
+    """Interface condition of an edge: cPINN -> normal-flux continuity
+    (Eq. 5); XPINN -> residual continuity (Eq. 6); hybrid (PAPER.md:948,
+    "cPINN in space + XPINN in time") -> flux on x1-normal edges, residual on
+    x2-normal (time) edges."""
+    if prob.method == "cpinn":
+        return True
+    if prob.method == "hybrid":
+        return normal[1] == 0.0
+    return False
+
+
 def interface_payload(prob, theta, X, normal, create_graph=True):
     """What subdomain q sends for one edge (Algorithm 1):
     u(x_I) [n, d_out] and f(x_I).n (cPINN) or F(x_I) (XPINN) [n, n_eq]."""
     fl, Xg = eval_fields(prob, theta, X, create_graph)
     u = torch.stack([f["u"] for f in fl], dim=1)
-    if prob.method == "cpinn":
+    if uses_flux(prob, normal):
         s = opde.flux_n(prob, fl, Xg, normal)
     else:
         s = opde.residual(prob, fl, Xg)

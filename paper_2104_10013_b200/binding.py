@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PINN_DD_LIB", os.path.join(_HERE, "libpinn_dd.so"))
 
 OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, ENONFINITE, EPROTOCOL = range(7)
-METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2}
+METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2, "hybrid": 3}
 PDES = {"burgers": 0, "poisson": 1, "heat": 2, "ns": 3}
 ACTS = {"tanh": 0, "sin": 1, "cos": 2}
 FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING = 1, 2, 4

@@ -381,7 +381,7 @@ struct KArgs {
   const float* coords;      // [2][n_points]
   const float* target;      // [DO][n_points]
   const float* mask;        // [DO][n_points]
-  const int32_t* pinfo;     // kind (bits 0-1: 0 residual, 1 data, 2 interface) | seg << 2
+  const int32_t* pinfo;     // kind (bits 0-1: 0 residual, 1 data, 2 interface) | flux (bit 2) | seg << 3
   const float* pinv;        // 1 / N of the point's class (per edge for interface points)
   const int32_t* ptwin;     // payload row of the twin (interface points)
   const float2* seg_normal; // [n_seg]
@@ -396,7 +396,7 @@ struct KArgs {
   float* payload;           // [rows][NF]
   float* gstash;            // global stash fallback (nullptr = TMEM)
   PdeConst pc;
-  int method;               // 0 pinn, 1 cpinn, 2 xpinn
+  int method;               // 0 pinn, 1 cpinn, 2 xpinn, 3 hybrid (per-edge choice in pinfo bit 2)
   float slope_n;
   float m1, m2;             // Laplacian mask (x1 in S, x2 in S)
 };

@@ -184,7 +184,7 @@ struct Layout {
 pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   if (!d) return fail(h, PINN_DD_EINVAL, "desc is NULL");
   if (d->d_in != 2) return fail(h, PINN_DD_EINVAL, "d_in must be 2 (got %d)", d->d_in);
-  if (d->method < 0 || d->method > 2) return fail(h, PINN_DD_EINVAL, "bad method %d", d->method);
+  if (d->method < 0 || d->method > 3) return fail(h, PINN_DD_EINVAL, "bad method %d", d->method);
   if (d->pde < 0 || d->pde > 3) return fail(h, PINN_DD_EINVAL, "bad pde %d", d->pde);
   const int want_do = d->pde == PINN_DD_PDE_NS ? 3 : 1;
   if (d->d_out != want_do) return fail(h, PINN_DD_EINVAL, "d_out %d does not match pde %d", d->d_out, d->pde);
@@ -522,8 +522,12 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
     int64_t p = off + nr + nd;
     for (int sgi = h->seg_off[q]; sgi < h->seg_off[q + 1]; ++sgi) {
       const int n = h->seg_n[sgi];
+      // interface condition of this edge: flux (cPINN, or HYBRID on an x1-normal
+      // edge) or residual (XPINN, or HYBRID on an x2-normal edge)
+      const bool flux = d->method == PINN_DD_METHOD_CPINN ||
+                        (d->method == PINN_DD_METHOD_HYBRID && h->seg_normal[2 * sgi + 1] == 0.0f);
       for (int j = 0; j < n; ++j, ++p) {
-        pinfo[p] = 2 | (sgi << 2);
+        pinfo[p] = 2 | (flux ? 4 : 0) | (sgi << 3);
         pinv[p] = 1.0f / float(n);
         ptwin[p] = int32_t(h->seg_twin[sgi] + j);
       }

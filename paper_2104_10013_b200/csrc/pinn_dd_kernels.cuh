@@ -406,8 +406,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           float r[3];
           float dr[3][DO][4];
           int ne;
-          if (a.method == 1) {
-            const float2 n = a.seg_normal[a.pinfo[gp] >> 2];
+          const int info = a.pinfo[gp];
+          if (info & 4) {
+            const float2 n = a.seg_normal[info >> 3];
             ne = pde_flux<DO>(a.pc, U, sX[p], sY[p], n.x, n.y, r, dr);
           } else {
             ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);
@@ -467,8 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
                 Ub[o].x += 0.5f * lw.z * inv * d;
               }
               int ne;
-              if (a.method == 1) {
-                const float2 n = a.seg_normal[info >> 2];
+              if (info & 4) {
+                const float2 n = a.seg_normal[info >> 3];
                 ne = pde_flux<DO>(a.pc, U, sX[p], sY[p], n.x, n.y, r, dr);
               } else {
                 ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);

@@ -142,7 +142,7 @@ class Subdomain:
 @dataclass
 class Problem:
     name: str
-    method: str                    # "pinn" | "cpinn" | "xpinn"
+    method: str                    # "pinn" | "cpinn" | "xpinn" | "hybrid" (flux in x1, residual in x2)
     pde: str                       # "burgers" | "poisson" | "heat" | "ns"
     activation: str                # "tanh" | "sin" | "cos"
     d_in: int
@@ -240,7 +240,7 @@ def build_problem(*, name: str, pde: str, method: str, nx: int, ny: int,
                   weights=(20.0, 1.0, 20.0, 20.0),
                   betas=(0.9, 0.999), eps: float = 1e-8,
                   n_f_per_sub: Optional[List[int]] = None) -> Problem:
-    if method not in ("pinn", "cpinn", "xpinn"):
+    if method not in ("pinn", "cpinn", "xpinn", "hybrid"):
         raise ValueError(method)
     d_out = PDE_OUTPUTS[pde]
     dlo = tuple(float(v) for v in domain_lo)

@@ -135,7 +135,7 @@ def test_cpinn_rejects_time_interfaces():
 
 
 @pytest.mark.parametrize("cfg,method", [("C1", "cpinn"), ("C2", "cpinn"), ("C2", "xpinn"),
-                                        ("C3", "xpinn"), ("C4", "xpinn"), ("C4", "cpinn")])
+                                        ("C3", "xpinn"), ("C3", "hybrid"), ("C4", "xpinn"), ("C4", "cpinn")])
 def test_gradient_matches_central_differences(cfg, method):
     """dJ_q/dTheta_q vs central differences of the literal loss (h = 1e-6),
     neighbours fixed.  This also pins reading Z1: the
@@ -248,3 +248,24 @@ def test_chunked_loss_terms_match_graph_loss(cfg, method):
         bd = OL.subdomain_loss_terms(p, q, th, chunk=7)
         ref = [float(x) for x in parts] + [float(J)]
         np.testing.assert_allclose(bd.as_list(), ref, rtol=1e-12, atol=1e-15)
+
+
+def test_hybrid_is_flux_in_space_residual_in_time():
+    """hybrid = cPINN flux continuity on x-normal edges + XPINN
+    residual continuity on t-normal edges; per-edge terms add up."""
+    p = perturb_params(_small("C3", method="hybrid", gpus=4), scale=0.2)
+    th = [torch.tensor(s.params) for s in p.subdomains]
+    pc = dataclasses.replace(p, method="cpinn")
+    px = dataclasses.replace(p, method="xpinn")
+    for q in range(4):
+        _, (mu, mf, ma, mi) = OL.subdomain_loss(p, q, th)
+        want = 0.0
+        for e in p.subdomains[q].edges:
+            ed = p.edges[e]
+            nb = p.edge_neighbor(q, e)
+            X = torch.tensor(ed.pts)
+            pp = pc if ed.axis == 0 else px
+            _, sq = OL.interface_payload(pp, th[q], X, ed.normal, create_graph=False)
+            _, sn = OL.interface_payload(pp, th[nb], X, ed.normal, create_graph=False)
+            want += float(((sq - sn) ** 2).sum()) / len(X)
+        assert float(mi) == pytest.approx(want, rel=1e-12)

@@ -108,6 +108,7 @@ CASES = [
     ("C3", dict(method="xpinn", gpus=1, n_f=300, n_u=50)),                  # single subdomain
     ("C4", dict(method="xpinn", n_f=150, n_i=20, n_u=16)),
     ("C4", dict(method="cpinn", n_f=150, n_i=20, n_u=16)),
+    ("C3", dict(method="hybrid", gpus=8, n_f=300, n_i=30, n_u=40)),   # P:948 cPINN-x + XPINN-t
 ]
 
 
@@ -129,7 +130,7 @@ def test_pinn_method_single_subdomain():
     run_parity(prob, "pinn")
 
 
-@pytest.mark.parametrize("cfg,kw", [CASES[3], CASES[2], CASES[7], CASES[8], CASES[0]])
+@pytest.mark.parametrize("cfg,kw", [CASES[3], CASES[2], CASES[7], CASES[8], CASES[0], CASES[9]])
 def test_payload_parity(cfg, kw):
     """K2: u(x_I) and f.n / F(x_I) of every local interface point."""
     prob = make_config(cfg, **kw)
