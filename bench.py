@@ -229,15 +229,28 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
-    prob = make_config("C2", method=args.method, weak=world)
-    owner = [s.ix // 4 for s in prob.subdomains]          # one 4x4 block per GPU
-    local = [q for q in range(prob.n_sub) if owner[q] == rank]
-    h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING)
+    if args.method == "dp":
+        # data-parallel vanilla PINN comparator: one 6x40 network on
+        # [0,G]x[0,1] with C2's point count per GPU, points sharded, gradient all-reduce
+        from paper_2104_10013_b200.binding import DataParallelPINN
+        prob = make_config("C2", method="pinn", weak=world, nx=1, ny=1,
+                           n_f=16 * 15000 * world, n_u=960 * world)
+        dp = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=FLAG_TIMING)
+        h = dp.h
+        h_prob, local = h.prob, [0]
+    else:
+        prob = make_config("C2", method=args.method, weak=world)
+        owner = [s.ix // 4 for s in prob.subdomains]          # one 4x4 block per GPU
+        local = [q for q in range(prob.n_sub) if owner[q] == rank]
+        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING)
+        h_prob = prob
     stream = h.stream
     pts_local = h.n_points
 
     def step():
-        if world == 1:
+        if args.method == "dp":
+            dp.step(1)
+        elif world == 1:
             h.step(1, want_loss=False)
         else:
             h.step_distributed(1, group)
@@ -288,7 +301,9 @@ def run_ours(args):
         h.coords.copy_(host[0], non_blocking=True)
         h.target.copy_(host[1], non_blocking=True)
         h.mask.copy_(host[2], non_blocking=True)
-        if world == 1:
+        if args.method == "dp":
+            loss = dp.step(1, want_loss=True)
+        elif world == 1:
             loss = h.step(1, want_loss=True)               # D2H of the loss breakdown (synchronises)
         else:
             loss = h.step_distributed(1, group, want_loss=True)   # D2H of the loss breakdown
@@ -299,7 +314,7 @@ def run_ours(args):
     e2e_val = float(pts_all.item()) * e2e_steps / float(e2e_s.item())
 
     # ---- roofline of the dominant kernel (K1, fused loss + grad)
-    k1_flops, k2_flops = algorithmic_flops(prob, local)
+    k1_flops, k2_flops = algorithmic_flops(h_prob, local)
     k1_ms = kt[1] / args.steps
     peak_fp32 = 148 * 128 * 2 * 1965e6 / 1e12              # TFLOP/s, FP32 FMA pipe at clocks.max.sm
     achieved = k1_flops / (k1_ms * 1e-3) / 1e12
@@ -312,14 +327,16 @@ def run_ours(args):
             traffic = None
 
     if rank == 0:
-        base = cpu_baseline(make_config("C2", method=args.method)) if (world == 1 and not args.no_cpu) else None
+        base = (cpu_baseline(make_config("C2", method=args.method)) if (world == 1 and not args.no_cpu
+                                                                       and args.method != "dp") else None)
         share = kt[1] / max(1e-9, sum(kt[:3]))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "iters_per_s": 1e3 * args.steps / t_max,
-            "config": {"workload": f"{prob.name} {prob.method}", "subdomains": prob.n_sub,
+            "config": {"workload": f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}",
+                       "subdomains": prob.n_sub,
                        "subdomains_per_gpu": len(local), "points_per_step": int(pts_all.item()),
                        "net": f"2-{prob.width}x{prob.n_hidden}-{prob.d_out} tanh, adaptive slope n=10",
                        "parallelism": f"domain decomposition, {len(local)} subdomains/GPU, P2P exchange",
@@ -351,7 +368,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--method", choices=["cpinn", "xpinn"], default="cpinn")
+    ap.add_argument("--method", choices=["cpinn", "xpinn", "hybrid", "dp"], default="cpinn",
+                    help="dp = data-parallel vanilla PINN comparator (Table 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

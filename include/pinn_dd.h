@@ -125,6 +125,11 @@ typedef struct {
   /* ---- runtime --------------------------------------------------------- */
   void* stream;              /* cudaStream_t (NULL = legacy default stream)        */
   int32_t flags;             /* PINN_DD_FLAG_*                                     */
+  /* ---- data-parallel shards (host, nullable) -------------------------- */
+  const int32_t* sub_norm_counts; /* [n_sub][2] (N_F, N_u) used for the 1/N of MSE_F and
+                                MSE_u instead of the local counts: a rank holding a shard of
+                                a subdomain's points then produces exactly its additive share
+                                of J and dJ/dTheta (sum over ranks = the full-data values). */
 } pinn_dd_desc;
 
 /* Number of packed parameters of one network [d_in, width x n_hidden, d_out]:

@@ -61,6 +61,7 @@ class Desc(C.Structure):
         ("n_points", C.c_int64), ("n_recv", C.c_int64),
         ("coords", C.c_void_p), ("target", C.c_void_p), ("mask", C.c_void_p), ("init_params", C.c_void_p),
         ("stream", C.c_void_p), ("flags", C.c_int32),
+        ("sub_norm_counts", C.POINTER(C.c_int32)),
     ]
 
 
@@ -205,7 +206,7 @@ def build_point_table(prob, local: Sequence[int], owner: Optional[Sequence[int]]
 
 
 def make_desc(prob, t: PointTable, dev_ptrs: Dict[str, int], stream: int = 0, flags: int = FLAG_GRAPH,
-              hparams: Optional[Sequence] = None):
+              hparams: Optional[Sequence] = None, norm_counts: Optional[Sequence] = None):
     """Fill a pinn_dd_desc; returns (desc, keep-alive list of host arrays)."""
     n_sub = len(t.local)
     if hparams is None:
@@ -237,6 +238,8 @@ def make_desc(prob, t: PointTable, dev_ptrs: Dict[str, int], stream: int = 0, fl
     d.init_params = dev_ptrs.get("init_params")
     d.stream = stream
     d.flags = flags
+    if norm_counts is not None:
+        d.sub_norm_counts = ptr(np.asarray(norm_counts, dtype=np.int32).reshape(-1), C.c_int32)
     return d, keep
 
 
@@ -244,7 +247,8 @@ class PinnDD:
     """One handle per GPU: the subdomains `local` of `prob`."""
 
     def __init__(self, prob, local: Optional[Sequence[int]] = None, owner: Optional[Sequence[int]] = None,
-                 rank: int = 0, device=None, flags: int = FLAG_GRAPH, hparams: Optional[Sequence] = None):
+                 rank: int = 0, device=None, flags: int = FLAG_GRAPH, hparams: Optional[Sequence] = None,
+                 norm_counts: Optional[Sequence] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("PinnDD needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
@@ -266,7 +270,7 @@ class PinnDD:
         self.stream = torch.cuda.current_stream(dev)
         d, self._keep = make_desc(prob, t, dict(coords=self.coords.data_ptr(), target=self.target.data_ptr(),
                                                mask=self.mask.data_ptr(), init_params=self.init_params.data_ptr()),
-                                  self.stream.cuda_stream, flags, hparams)
+                                  self.stream.cuda_stream, flags, hparams, norm_counts)
         self.desc = d
         nbytes = C.c_size_t(0)
         self._check(self.lib.pinn_dd_workspace_size(C.byref(d), C.byref(nbytes)), None)
@@ -399,3 +403,46 @@ def exchange_payload(payload: torch.Tensor, plan: ExchangePlan, group=None):
             ops.append(dist.P2POp(dist.irecv, payload[r0:r0 + n], peer, group))
     for req in dist.batch_isend_irecv(ops):
         req.wait()
+
+
+# ---------------------------------------------------------------------------
+# Data-parallel vanilla PINN (the paper's comparator, Fig. 1a / Table 2,
+# PAPER.md:38, 55, 737-768): one network replicated on every rank, the point
+# sets sharded, gradients summed with an all-reduce, identical Adam steps.
+# ---------------------------------------------------------------------------
+
+def shard_problem(prob, rank: int, world: int):
+    """Rank `rank`'s share (every world-th point) of a single-subdomain problem,
+    and the full-data counts (N_F, N_u) used for its 1/N normalisation."""
+    import dataclasses
+    if prob.n_sub != 1:
+        raise ValueError("data-parallel PINN shards a single network / subdomain")
+    s = prob.subdomains[0]
+    s2 = dataclasses.replace(s, x_f=s.x_f[rank::world], x_u=s.x_u[rank::world],
+                             u_target=s.u_target[rank::world], u_mask=s.u_mask[rank::world])
+    return dataclasses.replace(prob, subdomains=[s2]), (len(s.x_f), len(s.x_u))
+
+
+class DataParallelPINN:
+    """Each rank: loss + gradient of its shard (K1, K5a) -> all-reduce(sum) of the
+    gradient and loss breakdown -> Adam (K5b) on the summed gradient."""
+
+    def __init__(self, prob, rank: int = 0, world: int = 1, device=None, group=None, flags: int = 0):
+        shard, counts = shard_problem(prob, rank, world)
+        self.world, self.group = world, group
+        self.h = PinnDD(shard, device=device, flags=flags, norm_counts=[counts])
+
+    def step(self, n_iters: int = 1, want_loss: bool = False):
+        import torch.distributed as dist
+        loss = None
+        for _ in range(n_iters):
+            loss, grad = self.h.loss_grad()
+            if self.world > 1:
+                dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
+                dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=self.group)
+            self.h.set(0, grad[0], what=3)
+            self.h.adam()
+        return loss.cpu().numpy() if want_loss else None
+
+    def close(self):
+        self.h.close()

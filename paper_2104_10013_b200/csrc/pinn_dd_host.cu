@@ -105,7 +105,7 @@ const Ops* find_ops(int N, int NH, int DO, int ACT) {
 struct pinn_dd {
   // copied descriptor + owned host arrays
   pinn_dd_desc d;
-  std::vector<int32_t> sub_off, n_res, n_data, seg_off, seg_n;
+  std::vector<int32_t> sub_off, n_res, n_data, seg_off, seg_n, norm_counts;
   std::vector<int64_t> seg_twin;
   std::vector<float> seg_normal;
   std::vector<pinn_dd_hparams> hp;
@@ -208,6 +208,12 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   if (d->sub_point_offset[d->n_sub] != d->n_points)
     return fail(h, PINN_DD_EINVAL, "sub_point_offset[n_sub] != n_points");
   if (d->sub_seg_offset[d->n_sub] != d->n_seg) return fail(h, PINN_DD_EINVAL, "sub_seg_offset[n_sub] != n_seg");
+  if (d->sub_norm_counts)
+    for (int q = 0; q < d->n_sub; ++q)
+      if (d->sub_norm_counts[2 * q] < d->sub_n_res[q] || d->sub_norm_counts[2 * q + 1] < d->sub_n_data[q] ||
+          (d->sub_n_res[q] > 0 && d->sub_norm_counts[2 * q] <= 0) ||
+          (d->sub_n_data[q] > 0 && d->sub_norm_counts[2 * q + 1] <= 0))
+        return fail(h, PINN_DD_EINVAL, "subdomain %d: normalisation counts below the local counts", q);
   bool any_data = false;
   for (int q = 0; q < d->n_sub; ++q) {
     const int64_t cnt = int64_t(d->sub_point_offset[q + 1]) - d->sub_point_offset[q];
@@ -464,6 +470,7 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->n_data.assign(d->sub_n_data, d->sub_n_data + ns);
   h->seg_off.assign(d->sub_seg_offset, d->sub_seg_offset + ns + 1);
   h->hp.assign(d->sub_hparams, d->sub_hparams + ns);
+  if (d->sub_norm_counts) h->norm_counts.assign(d->sub_norm_counts, d->sub_norm_counts + 2 * ns);
   if (d->n_seg > 0) {
     h->seg_n.assign(d->seg_n, d->seg_n + d->n_seg);
     h->seg_twin.assign(d->seg_twin, d->seg_twin + d->n_seg);
@@ -477,6 +484,7 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->d.seg_n = h->seg_n.data();
   h->d.seg_twin = h->seg_twin.data();
   h->d.seg_normal = h->seg_normal.data();
+  h->d.sub_norm_counts = d->sub_norm_counts ? h->norm_counts.data() : nullptr;
   h->stream = static_cast<cudaStream_t>(d->stream);
 
   char* base = static_cast<char*>(ws);
@@ -511,13 +519,16 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   for (int q = 0; q < ns; ++q) {
     const int64_t off = h->sub_off[q];
     const int nr = h->n_res[q], nd = h->n_data[q];
+    // 1/N of MSE_F and MSE_u: local counts, or the full-data counts of a shard
+    const int cr = h->norm_counts.empty() ? nr : h->norm_counts[2 * q];
+    const int cd = h->norm_counts.empty() ? nd : h->norm_counts[2 * q + 1];
     for (int64_t p = off; p < off + nr; ++p) {
       pinfo[p] = 0;
-      pinv[p] = 1.0f / float(nr);
+      pinv[p] = 1.0f / float(cr);
     }
     for (int64_t p = off + nr; p < off + nr + nd; ++p) {
       pinfo[p] = 1;
-      pinv[p] = 1.0f / float(nd);
+      pinv[p] = 1.0f / float(cd);
     }
     int64_t p = off + nr + nd;
     for (int sgi = h->seg_off[q]; sgi < h->seg_off[q + 1]; ++sgi) {
@@ -616,9 +627,27 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   return PINN_DD_OK;
 }
 
+// per-call timing of the phased entry points (PINN_DD_FLAG_TIMING): events 4/5
+static pinn_dd_status phase_begin(pinn_dd* h) {
+  if (h->d.flags & PINN_DD_FLAG_TIMING) CK(h, cudaEventRecord(h->ev[4], h->stream));
+  return PINN_DD_OK;
+}
+static pinn_dd_status phase_end(pinn_dd* h, int slot) {
+  if (h->d.flags & PINN_DD_FLAG_TIMING) {
+    CK(h, cudaEventRecord(h->ev[5], h->stream));
+    CK(h, cudaEventSynchronize(h->ev[5]));
+    float ms = 0;
+    CK(h, cudaEventElapsedTime(&ms, h->ev[4], h->ev[5]));
+    h->ms[slot] += ms;
+  }
+  return PINN_DD_OK;
+}
+
 pinn_dd_status pinn_dd_interface_payload(pinn_dd* h) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
-  return launch_k2(h);
+  pinn_dd_status s;
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k2(h)) != PINN_DD_OK) return s;
+  return phase_end(h, 0);
 }
 
 pinn_dd_status pinn_dd_payload_buffer(pinn_dd* h, float** buf, int32_t* n_fields, int64_t* n_rows) {
@@ -632,8 +661,10 @@ pinn_dd_status pinn_dd_payload_buffer(pinn_dd* h, float** buf, int32_t* n_fields
 pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
   pinn_dd_status s;
-  if ((s = launch_k1(h)) != PINN_DD_OK) return s;
-  if ((s = launch_k5(h, 0)) != PINN_DD_OK) return s;
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h)) != PINN_DD_OK || (s = phase_end(h, 1)) != PINN_DD_OK)
+    return s;
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k5(h, 0)) != PINN_DD_OK || (s = phase_end(h, 2)) != PINN_DD_OK)
+    return s;
   if (loss_dev)
     CK(h, cudaMemcpyAsync(loss_dev, h->loss, size_t(h->d.n_sub) * 8 * 4, cudaMemcpyDeviceToDevice, h->stream));
   if (grad_dev) {
@@ -647,7 +678,9 @@ pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev) {
 
 pinn_dd_status pinn_dd_adam(pinn_dd* h) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
-  return launch_k5(h, 2);
+  pinn_dd_status s;
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k5(h, 2)) != PINN_DD_OK) return s;
+  return phase_end(h, 2);
 }
 
 pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
