@@ -42,8 +42,13 @@ def _mse_sum(r: torch.Tensor) -> torch.Tensor:
     return (r * r).sum() / r.shape[0]
 
 
-def eval_fields(prob, theta, X, create_graph=True):
-    fl, Xg = onet.fields(theta, prob.sizes, X, prob.activation, prob.slope_n,
+def _act(prob, q):
+    """Activation of subdomain q (per region in C5, Table 3)."""
+    return prob.act(q) if q is not None else prob.activation
+
+
+def eval_fields(prob, theta, X, create_graph=True, q=None):
+    fl, Xg = onet.fields(theta, prob.sizes, X, _act(prob, q), prob.slope_n,
                          second=opde.SECOND[prob.pde], create_graph=create_graph)
     return fl, Xg
 
@@ -60,10 +65,10 @@ def uses_flux(prob, normal) -> bool:
     return False
 
 
-def interface_payload(prob, theta, X, normal, create_graph=True):
+def interface_payload(prob, theta, X, normal, create_graph=True, q=None):
     """What subdomain q sends for one edge (Algorithm 1):
     u(x_I) [n, d_out] and f(x_I).n (cPINN) or F(x_I) (XPINN) [n, n_eq]."""
-    fl, Xg = eval_fields(prob, theta, X, create_graph)
+    fl, Xg = eval_fields(prob, theta, X, create_graph, q)
     u = torch.stack([f["u"] for f in fl], dim=1)
     if uses_flux(prob, normal):
         s = opde.flux_n(prob, fl, Xg, normal)
@@ -100,13 +105,13 @@ def subdomain_loss(prob, q: int, thetas: Sequence[torch.Tensor],
     # MSE_F : residual points
     X_f = _t(s.x_f)
     if len(X_f):
-        fl, Xg = eval_fields(prob, th, X_f)
+        fl, Xg = eval_fields(prob, th, X_f, q=q)
         mse_f = _mse_sum(opde.residual(prob, fl, Xg))
     else:
         mse_f = torch.zeros((), dtype=DT)
     # MSE_u : training points, masked outputs
     if len(s.x_u):
-        u = onet.forward(th, prob.sizes, _t(s.x_u), prob.activation, prob.slope_n)
+        u = onet.forward(th, prob.sizes, _t(s.x_u), _act(prob, q), prob.slope_n)
         mse_u = _mse_sum(_t(s.u_mask) * (_t(s.u_target) - u))
     else:
         mse_u = torch.zeros((), dtype=DT)
@@ -117,12 +122,12 @@ def subdomain_loss(prob, q: int, thetas: Sequence[torch.Tensor],
         ed = prob.edges[e]
         nb = prob.edge_neighbor(q, e)
         X_i = _t(ed.pts)
-        u_q, s_q = interface_payload(prob, th, X_i, ed.normal)
+        u_q, s_q = interface_payload(prob, th, X_i, ed.normal, q=q)
         if payloads is not None:
             u_n, s_n = payloads[(nb, e)]
         else:
             u_n, s_n = interface_payload(prob, thetas[nb].detach(), X_i, ed.normal,
-                                         create_graph=False)
+                                         create_graph=False, q=nb)
         uavg = 0.5 * (u_q + u_n)                      # {{u}}
         mse_uavg = mse_uavg + _mse_sum(u_q - uavg)
         mse_if = mse_if + _mse_sum(s_q - s_n)
@@ -139,13 +144,13 @@ def subdomain_loss_terms(prob, q: int, thetas: Sequence[torch.Tensor], chunk: in
     sq = torch.zeros((), dtype=DT)
     X_f = _t(s.x_f)
     for i in range(0, len(X_f), chunk):
-        fl, Xg = eval_fields(prob, th, X_f[i:i + chunk], create_graph=False)
+        fl, Xg = eval_fields(prob, th, X_f[i:i + chunk], create_graph=False, q=q)
         r = opde.residual(prob, fl, Xg).detach()
         sq = sq + (r * r).sum()
     mse_f = sq / len(X_f) if len(X_f) else torch.zeros((), dtype=DT)
     with torch.no_grad():
         if len(s.x_u):
-            u = onet.forward(th, prob.sizes, _t(s.x_u), prob.activation, prob.slope_n)
+            u = onet.forward(th, prob.sizes, _t(s.x_u), _act(prob, q), prob.slope_n)
             mse_u = _mse_sum(_t(s.u_mask) * (_t(s.u_target) - u))
         else:
             mse_u = torch.zeros((), dtype=DT)
@@ -155,8 +160,9 @@ def subdomain_loss_terms(prob, q: int, thetas: Sequence[torch.Tensor], chunk: in
         ed = prob.edges[e]
         nb = prob.edge_neighbor(q, e)
         X_i = _t(ed.pts)
-        u_q, s_q = interface_payload(prob, th, X_i, ed.normal, create_graph=False)
-        u_n, s_n = interface_payload(prob, thetas[nb].detach(), X_i, ed.normal, create_graph=False)
+        u_q, s_q = interface_payload(prob, th, X_i, ed.normal, create_graph=False, q=q)
+        u_n, s_n = interface_payload(prob, thetas[nb].detach(), X_i, ed.normal, create_graph=False,
+                                     q=nb)
         mse_uavg = mse_uavg + _mse_sum(u_q - 0.5 * (u_q + u_n))
         mse_if = mse_if + _mse_sum(s_q - s_n)
     total = prob.w_u * mse_u + prob.w_f * mse_f + prob.w_i * mse_uavg + prob.w_if * mse_if
@@ -179,7 +185,7 @@ def all_payloads(prob, thetas):
     for e, ed in enumerate(prob.edges):
         for q in (ed.a, ed.b):
             pay[(q, e)] = interface_payload(prob, thetas[q].detach(), _t(ed.pts), ed.normal,
-                                            create_graph=False)
+                                            create_graph=False, q=q)
     return pay
 
 
@@ -261,6 +267,6 @@ def stitch(prob, thetas, X: np.ndarray) -> torch.Tensor:
         w = torch.tensor([1.0 / len(o) if q in o else 0.0 for o in own], dtype=DT)
         if float(w.abs().sum()) == 0.0:
             continue
-        uq = onet.forward(thetas[q].detach(), prob.sizes, Xt, prob.activation, prob.slope_n)
+        uq = onet.forward(thetas[q].detach(), prob.sizes, Xt, _act(prob, q), prob.slope_n)
         u = u + w[:, None] * uq
     return u

@@ -22,9 +22,10 @@ SECOND = {
     "poisson": (True, True),
     "heat": (True, True),
     "ns": (True, True),
+    "heat_inv": (True, True),
 }
 
-N_EQ = {"burgers": 1, "poisson": 1, "heat": 1, "ns": 3}
+N_EQ = {"burgers": 1, "poisson": 1, "heat": 1, "ns": 3, "heat_inv": 1}
 
 
 # --------------------------------------------------------------------------
@@ -94,6 +95,24 @@ def heat_flux_n(fl, X, n):
 
 
 # --------------------------------------------------------------------------
+# Inverse heat conduction, Eq. (15) with K unknown: one net
+# per region with outputs (T, K) (reading Z17'), F = d_x(K T_x) + d_y(K T_y) - f
+# with both T and K from the net, f = 4 exp(-0.1 y) of the exact pair
+# T* = 20 exp(-0.1 y), K* = 20 + exp(0.1 y) sin(0.5 x).
+# --------------------------------------------------------------------------
+
+def heat_inv_residual(fl, X):
+    T, K = fl
+    return (K["u"] * (T["d11"] + T["d22"]) + K["d1"] * T["d1"] + K["d2"] * T["d2"]
+            - heat_forcing(X))[:, None]
+
+
+def heat_inv_flux_n(fl, X, n):
+    T, K = fl
+    return (K["u"] * (T["d1"] * n[0] + T["d2"] * n[1]))[:, None]
+
+
+# --------------------------------------------------------------------------
 # Steady incompressible NS, Eq. (11) and Table 1 fluxes
 # --------------------------------------------------------------------------
 
@@ -130,6 +149,8 @@ def residual(prob, fl, X):
         return heat_residual(fl, X)
     if prob.pde == "ns":
         return ns_residual(fl, X, prob.re)
+    if prob.pde == "heat_inv":
+        return heat_inv_residual(fl, X)
     raise ValueError(prob.pde)
 
 
@@ -142,4 +163,6 @@ def flux_n(prob, fl, X, n):
         return heat_flux_n(fl, X, n)
     if prob.pde == "ns":
         return ns_flux_n(fl, X, n, prob.re)
+    if prob.pde == "heat_inv":
+        return heat_inv_flux_n(fl, X, n)
     raise ValueError(prob.pde)

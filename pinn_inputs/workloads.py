@@ -32,7 +32,7 @@ import numpy as np
 
 SEED_BASE = 2104_10013
 
-PDE_OUTPUTS = {"burgers": 1, "poisson": 1, "heat": 1, "ns": 3}
+PDE_OUTPUTS = {"burgers": 1, "poisson": 1, "heat": 1, "ns": 3, "heat_inv": 2}
 
 
 def _f32(a) -> np.ndarray:
@@ -137,13 +137,14 @@ class Subdomain:
     u_mask: np.ndarray             # [N_u, d_out] 1 = constrained output, 0 = free
     edges: List[int]               # ids of the live interface edges, ascending
     params: np.ndarray             # flat initial parameters (layer-major)
+    activation: Optional[str] = None   # per-subdomain activation (C5, Table 3); None = problem's
 
 
 @dataclass
 class Problem:
     name: str
     method: str                    # "pinn" | "cpinn" | "xpinn" | "hybrid" (flux in x1, residual in x2)
-    pde: str                       # "burgers" | "poisson" | "heat" | "ns"
+    pde: str                       # "burgers" | "poisson" | "heat" | "ns" | "heat_inv"
     activation: str                # "tanh" | "sin" | "cos"
     d_in: int
     d_out: int
@@ -166,6 +167,7 @@ class Problem:
     domain_hi: Tuple[float, float]
     subdomains: List[Subdomain]
     edges: List[Edge]
+    meta: Dict = field(default_factory=dict)   # generator geometry (C5: seeds, polygon)
 
     @property
     def sizes(self) -> List[int]:
@@ -182,6 +184,11 @@ class Problem:
             tot += len(s.x_f) + len(s.x_u)
             tot += sum(len(self.edges[e].pts) for e in s.edges)
         return tot
+
+    def act(self, q: int) -> str:
+        """Activation of subdomain q (Table 3 gives one per region)."""
+        a = self.subdomains[q].activation
+        return self.activation if a is None else a
 
     def edge_neighbor(self, q: int, e: int) -> int:
         ed = self.edges[e]
@@ -222,6 +229,15 @@ def _targets(pde: str, x: np.ndarray, tag: str) -> Tuple[np.ndarray, np.ndarray]
     if pde == "heat":
         t = 20.0 * np.exp(-0.1 * x[:, 1])
         return t[:, None], np.ones((n, 1))
+    if pde == "heat_inv":
+        # outputs (T, K): T* = 20 exp(-0.1 y), K* = 20 + exp(0.1 y) sin(0.5 x)
+        # (PAPER.md:828-829).  "interior": T data only; "boundary": T and K.
+        tgt = np.stack([20.0 * np.exp(-0.1 * x[:, 1]),
+                        20.0 + np.exp(0.1 * x[:, 1]) * np.sin(0.5 * x[:, 0])], axis=1)
+        mask = np.ones((n, 2))
+        if tag == "interior":
+            mask[:, 1] = 0.0
+        return tgt, mask
     if pde == "ns":
         tgt = np.zeros((n, 3))
         if tag == "x2hi":
@@ -354,7 +370,92 @@ def _c4(scale, method=None, **kw):
                 n_f=125000, n_i=250, n_u=80, width=80, n_hidden=5, lr=6e-4, seed_index=3)
 
 
-CONFIGS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4}
+# C5 (NEXT row f1): inverse heat conduction, XPINN on 10 seeded-Voronoi
+# regions of a non-convex map polygon (Table 3).
+C5_N_F = [3000, 4000, 5000, 4000, 3000, 4000, 800, 3000, 5000, 4000]   # Table 3
+C5_ACT = ["tanh", "sin", "cos", "tanh", "sin", "cos", "tanh", "sin", "cos", "tanh"]
+
+
+def _c5(scale, method=None, **kw):
+    return dict(name="C5-heatinv-xpinn-voronoi10-3x80", pde="heat_inv", method=method or "xpinn",
+                n_f=C5_N_F, n_i=100, n_u=400, width=80, n_hidden=3, lr=6e-3, seed_index=4,
+                t_frac=0.1)
+
+
+def build_voronoi_problem(*, name: str, pde: str, method: str, n_f, n_i: int, n_u: int,
+                          width: int, n_hidden: int, lr: float, seed_index: int,
+                          t_frac: float = 0.1, activations=None, n_regions: int = 10,
+                          slope_n: float = 10.0, weights=(20.0, 1.0, 20.0, 20.0),
+                          betas=(0.9, 0.999), eps: float = 1e-8, **_) -> Problem:
+    """C5 recipe (reading Z24): regions = nearest-seed cells of Lloyd-relaxed
+    seeds inside `voronoi.MAP_POLYGON`; N_F(q) uniform residual points in
+    region q (Table 3); round(t_frac N_F(q)) interior T-only data points;
+    `n_u` boundary points uniform in arc length, each assigned to its region,
+    with T and K data; per Voronoi interface segment, N_I points at the
+    midpoints of N_I equal sub-segments (split over the segments of a pair in
+    proportion to length)."""
+    from . import voronoi as vor
+    if pde != "heat_inv":
+        raise ValueError(pde)
+    d_out = PDE_OUTPUTS[pde]
+    poly = vor.MAP_POLYGON
+    root = np.random.SeedSequence(SEED_BASE + seed_index)
+    seqs = root.spawn(2 + n_regions)
+    grng, brng = np.random.default_rng(seqs[0]), np.random.default_rng(seqs[1])
+    seeds = vor.lloyd_seeds(poly, n_regions, grng)
+    acts = activations or C5_ACT
+    # interfaces
+    edges: List[Edge] = []
+    if method != "pinn":
+        segs = vor.interface_segments(poly, seeds)
+        pairs = {}
+        for s in segs:
+            pairs.setdefault((s[0], s[1]), []).append(s)
+        for (a, b), ss in sorted(pairs.items()):
+            lens = np.array([np.linalg.norm(s[3] - s[2]) for s in ss])
+            cnt = np.floor(n_i * lens / lens.sum()).astype(int)
+            cnt[: n_i - cnt.sum()] += 1
+            for (_, _, p0, p1, nrm), c in zip(ss, cnt):
+                if c == 0:
+                    continue
+                f = (np.arange(c) + 0.5) / c
+                pts = p0[None, :] + f[:, None] * (p1 - p0)[None, :]
+                edges.append(Edge(len(edges), a, b, -1, (float(nrm[0]), float(nrm[1])), _f32(pts)))
+    elif n_regions != 1:
+        raise ValueError("method 'pinn' needs a single subdomain")
+    # boundary data, assigned to regions
+    xb = vor.boundary_sample(poly, n_u, brng) if n_u > 0 else np.zeros((0, 2))
+    xb = _f32(xb)
+    lab_b = vor.nearest(seeds, xb) if len(xb) else np.zeros(0, dtype=int)
+    sizes = layer_sizes(2, width, n_hidden, d_out)
+    subs: List[Subdomain] = []
+    for q in range(n_regions):
+        prng, wrng = [np.random.default_rng(s) for s in seqs[2 + q].spawn(2)]
+        nf = n_f[q] if isinstance(n_f, (list, tuple)) else n_f
+        x_f = _f32(vor.sample_region(poly, seeds, q, nf, prng))
+        nt = int(round(t_frac * nf))
+        x_t = _f32(vor.sample_region(poly, seeds, q, nt, prng)) if nt > 0 else np.zeros((0, 2))
+        t_t, m_t = _targets(pde, x_t, "interior")
+        x_b = xb[lab_b == q]
+        t_b, m_b = _targets(pde, x_b, "boundary")
+        x_u = np.concatenate([x_t, x_b])
+        lo, hi = tuple(x_f.min(0)), tuple(x_f.max(0))
+        my_edges = [e.id for e in edges if e.a == q or e.b == q]
+        subs.append(Subdomain(q, q, 0, lo, hi, x_f, _f32(x_u), _f32(np.concatenate([t_t, t_b])),
+                              _f32(np.concatenate([m_t, m_b])), my_edges,
+                              xavier_params(sizes, slope_n, wrng), activation=acts[q]))
+    f = lambda v: float(np.float32(v))
+    dlo, dhi = tuple(poly.min(0)), tuple(poly.max(0))
+    return Problem(name=name, method=method, pde=pde, activation=acts[0], d_in=2,
+                   d_out=d_out, width=width, n_hidden=n_hidden, slope_n=f(slope_n),
+                   nu=0.0, re=f(100.0), w_u=f(weights[0]), w_f=f(weights[1]),
+                   w_i=f(weights[2]), w_if=f(weights[3]), lr=f(lr),
+                   beta1=f(betas[0]), beta2=f(betas[1]), eps=f(eps),
+                   nx=n_regions, ny=1, domain_lo=dlo, domain_hi=dhi, subdomains=subs, edges=edges,
+                   meta={"seeds": seeds, "polygon": poly})
+
+
+CONFIGS = {"C1": _c1, "C2": _c2, "C3": _c3, "C4": _c4, "C5": _c5}
 
 
 def make_config(cfg: str, *, scale: float = 1.0, method: Optional[str] = None,
@@ -368,12 +469,18 @@ def make_config(cfg: str, *, scale: float = 1.0, method: Optional[str] = None,
         if val is not None:
             args[key] = val
         elif scale != 1.0:
-            args[key] = max(1 if key != "n_u" else 0, int(round(args[key] * scale)))
+            lo = 1 if key != "n_u" else 0
+            v = args[key]
+            args[key] = ([max(lo, int(round(x * scale))) for x in v] if isinstance(v, list)
+                         else max(lo, int(round(v * scale))))
     if width is not None:
         args["width"] = width
     if n_hidden is not None:
         args["n_hidden"] = n_hidden
-    for k in ("nx", "ny", "activation", "weights", "lr", "slope_n", "nu", "re", "pde", "seed_index"):
+    for k in ("nx", "ny", "activation", "weights", "lr", "slope_n", "nu", "re", "pde", "seed_index",
+              "activations", "t_frac"):
         if k in kw:
             args[k] = kw[k]
+    if cfg == "C5":
+        return build_voronoi_problem(**args)
     return build_problem(**args)

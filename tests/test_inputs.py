@@ -61,3 +61,57 @@ def test_init_slopes():
     for ent in param_layout(p.sizes):
         if "a" in ent:
             assert all(np.float32(s.params[ent["a"][0]]) == np.float32(0.1) for s in p.subdomains)
+
+
+def _segments_cross(p, q, r, s):
+    d = lambda a, b, c: (b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0])
+    return (d(p, q, r) * d(p, q, s) < 0) and (d(r, s, p) * d(r, s, q) < 0)
+
+
+def test_c5_voronoi_geometry():
+    """C5 recipe (reading Z24): simple non-convex polygon; residual points in
+    their own region; interface points on the bisector of their two seeds
+    with no third seed nearer; boundary data on the polygon boundary."""
+    from pinn_inputs import voronoi as vor
+    from pinn_inputs.workloads import C5_ACT, C5_N_F
+    P = vor.MAP_POLYGON
+    n = len(P)
+    for i in range(n):
+        for j in range(i + 2, n):
+            if (j + 1) % n == i:
+                continue
+            assert not _segments_cross(P[i], P[(i + 1) % n], P[j], P[(j + 1) % n])
+    e = np.roll(P, -1, 0) - P
+    cr = e[:, 0] * np.roll(e, -1, 0)[:, 1] - e[:, 1] * np.roll(e, -1, 0)[:, 0]
+    assert (cr > 0).any() and (cr < 0).any()          # non-convex
+    p = make_config("C5", scale=0.1)
+    seeds = p.meta["seeds"]
+    assert [s.activation for s in p.subdomains] == C5_ACT
+    assert [len(s.x_f) for s in p.subdomains] == [round(0.1 * v) for v in C5_N_F]
+    for s in p.subdomains:
+        assert vor.inside(P, s.x_f).all()
+        assert (vor.nearest(seeds, s.x_f) == s.id).all()
+    assert len(p.edges) >= 9                           # a connected 10-region partition
+    for ed in p.edges:
+        x = ed.pts
+        da = np.linalg.norm(x - seeds[ed.a], axis=1)
+        db = np.linalg.norm(x - seeds[ed.b], axis=1)
+        np.testing.assert_allclose(da, db, rtol=0, atol=2e-6)
+        dmin = np.min(np.linalg.norm(x[:, None, :] - seeds[None], axis=2), axis=1)
+        assert np.all(dmin >= da - 2e-6)
+        assert vor.inside(P, x).all()
+        nrm = np.array(ed.normal)
+        assert abs(np.linalg.norm(nrm) - 1.0) < 1e-6
+        np.testing.assert_allclose(np.abs((x[1:] - x[:-1]) @ nrm), 0.0, atol=2e-6)
+    # boundary data carry K; interior data do not
+    nb = 0
+    for s in p.subdomains:
+        kb = s.u_mask[:, 1] == 1.0
+        nb += kb.sum()
+        xb = s.x_u[kb]
+        if len(xb):
+            a, b = P[None, :, :], np.roll(P, -1, 0)[None, :, :]
+            t = np.clip((((xb[:, None] - a) * (b - a)).sum(-1)) / ((b - a) ** 2).sum(-1), 0, 1)
+            dist = np.linalg.norm(xb[:, None] - (a + t[..., None] * (b - a)), axis=2).min(1)
+            assert dist.max() < 1e-5
+    assert nb == round(0.1 * 400)

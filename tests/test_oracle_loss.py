@@ -106,10 +106,13 @@ def test_single_subdomain_degenerates_to_pinn(cfg):
 
 
 @pytest.mark.parametrize("cfg,method", [("C1", "cpinn"), ("C2", "cpinn"), ("C2", "xpinn"),
-                                        ("C3", "xpinn"), ("C4", "xpinn"), ("C4", "cpinn")])
+                                        ("C3", "xpinn"), ("C4", "xpinn"), ("C4", "cpinn"),
+                                        ("C5", "xpinn"), ("C5", "cpinn")])
 def test_identical_neighbours_have_zero_interface_loss(cfg, method):
-    """{{u}} = (u_q + u_q+)/2: identical nets give MSE_uavg = MSE_flux = MSE_R = 0 exactly."""
-    p = _small(cfg, method=method)
+    """{{u}} = (u_q + u_q+)/2: identical nets give MSE_uavg = MSE_flux = MSE_R = 0 exactly
+    (C5: with one activation everywhere -- identical parameters are identical nets)."""
+    kw = dict(activations=["sin"] * 10) if cfg == "C5" else {}
+    p = _small(cfg, method=method, **kw)
     p = _with_params(p, [p.subdomains[0].params] * p.n_sub)
     th = [torch.tensor(s.params) for s in p.subdomains]
     for q in range(p.n_sub):
@@ -135,19 +138,25 @@ def test_cpinn_rejects_time_interfaces():
 
 
 @pytest.mark.parametrize("cfg,method", [("C1", "cpinn"), ("C2", "cpinn"), ("C2", "xpinn"),
-                                        ("C3", "xpinn"), ("C3", "hybrid"), ("C4", "xpinn"), ("C4", "cpinn")])
+                                        ("C3", "xpinn"), ("C3", "hybrid"), ("C4", "xpinn"), ("C4", "cpinn"),
+                                        ("C5", "xpinn"), ("C5-sin", "xpinn"), ("C5-cos", "xpinn")])
 def test_gradient_matches_central_differences(cfg, method):
     """dJ_q/dTheta_q vs central differences of the literal loss (h = 1e-6),
     neighbours fixed.  This also pins reading Z1: the
-    u_q inside {{u}} is differentiated."""
+    u_q inside {{u}} is differentiated.  C5 variants put a tanh / sin / cos
+    region last (its neighbours keep Table 3's mixed activations)."""
     kw = dict(n_f=10, n_i=4, n_u=5, width=4, n_hidden=2)
     if cfg == "C3":
         kw["gpus"] = 4
+    if cfg.startswith("C5"):
+        last = cfg[3:] or "tanh"
+        kw["activations"] = ["tanh", "sin", "cos", "tanh", "sin", "cos", "tanh", "sin", "cos", last]
+        cfg = "C5"
     p = perturb_params(make_config(cfg, method=method, **kw), scale=0.2)
     th = [torch.tensor(s.params) for s in p.subdomains]
     q = p.n_sub - 1
     _, g = OL.loss_and_grad(p, q, th)
-    h = 1e-6
+    h = 1e-5 if p.pde == "heat_inv" else 1e-6   # C5: J ~ 1e4 (T, K ~ 20), so rounding needs a larger h
     fd = np.zeros(len(g))
     for i in range(len(g)):
         tp = [t.clone() for t in th]; tm = [t.clone() for t in th]
@@ -159,7 +168,7 @@ def test_gradient_matches_central_differences(cfg, method):
     assert err < 1e-6, err
 
 
-@pytest.mark.parametrize("cfg,method", [("C1", "cpinn"), ("C2", "xpinn"), ("C4", "cpinn")])
+@pytest.mark.parametrize("cfg,method", [("C1", "cpinn"), ("C2", "xpinn"), ("C4", "cpinn"), ("C5", "xpinn")])
 def test_slope_gradient_homogeneity_identity(cfg, method):
     """J depends on (a^k, W^k, b^k) only through (n a^k W^k, n a^k b^k) (Eq. 2 with
     the slope inside Phi), hence a^k dJ/da^k = <W^k, dJ/dW^k> + <b^k, dJ/db^k>

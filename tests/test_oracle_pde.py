@@ -170,3 +170,60 @@ def test_inputs_targets_match_paper_conditions():
         assert ic.sum() == 50
         np.testing.assert_allclose(s.u_target[ic, 0], -np.sin(np.pi * s.x_u[ic, 0]), atol=1e-7)
         assert np.all(s.u_target[~ic, 0] == 0) and np.all(np.abs(s.x_u[~ic, 0]) == 1.0)
+
+
+# --------------------------------------------------------------------------
+# inverse heat (C5): one net with outputs (T, K) (reading Z17')
+# --------------------------------------------------------------------------
+
+def _tk(X):
+    return (lambda X: 20.0 * torch.exp(-0.1 * X[:, 1]),
+            lambda X: 20.0 + torch.exp(0.1 * X[:, 1]) * torch.sin(0.5 * X[:, 0]))
+
+
+def test_heat_inv_paper_pair_vanishes():
+    # the exact (T, K) pair satisfies d_x(K T_x) + d_y(K T_y) = f
+    X = _pts(1000, (0, 0), (10, 6), seed=3)
+    fl, Xg = _autograd_fields(list(_tk(X)), X)
+    assert opde.heat_inv_residual(fl, Xg).abs().max() < 1e-12
+    # T_x = 0, so K = 20 + C e^{0.1 y} solves it too (reading Z22, identifiability):
+    # K = 20 gives 0; K = 25 gives F = 25 * 0.2 e^{-0.1 y} - 4 e^{-0.1 y} = e^{-0.1 y}
+    for c, want in ((20.0, 0.0), (25.0, 1.0)):
+        fl2, Xg2 = _autograd_fields([_tk(X)[0], lambda X, c=c: c + 0.0 * X[:, 0] * X[:, 1]], X)
+        F = opde.heat_inv_residual(fl2, Xg2)[:, 0]
+        assert torch.allclose(F, want * torch.exp(-0.1 * X[:, 1]), rtol=1e-12, atol=1e-12)
+
+
+def test_heat_inv_is_divergence_of_flux_and_reduces_to_heat():
+    """For arbitrary smooth T and K: the expanded residual equals
+    div(K grad T) - f by autograd (pins which output is T and which is K and
+    the K_x T_x + K_y T_y cross terms); the flux with n = e1, e2 is K T_x,
+    K T_y; with K = the known heat_K it equals the forward heat residual."""
+    X = _pts(300, (0, 0), (4, 3), seed=9)
+    Tf = lambda X: X[:, 0] ** 2 * X[:, 1] + torch.sin(X[:, 0]) * torch.cos(0.7 * X[:, 1])
+    Kf = lambda X: 3.0 + X[:, 0] * X[:, 1] ** 2 + torch.cos(0.3 * X[:, 0])
+    Xr = X.clone().requires_grad_(True)
+    T, K = Tf(Xr), Kf(Xr)
+    g = torch.autograd.grad(T.sum(), Xr, create_graph=True)[0]
+    div = torch.autograd.grad((K * g[:, 0]).sum(), Xr, create_graph=True)[0][:, 0] + \
+        torch.autograd.grad((K * g[:, 1]).sum(), Xr, create_graph=True)[0][:, 1]
+    ref = (div - 4.0 * torch.exp(-0.1 * Xr[:, 1])).detach()
+    fl, Xg = _autograd_fields([Tf, Kf], X)
+    assert torch.allclose(opde.heat_inv_residual(fl, Xg)[:, 0], ref, rtol=1e-12, atol=1e-11)
+    fx = opde.heat_inv_flux_n(fl, Xg, (1.0, 0.0))[:, 0]
+    fy = opde.heat_inv_flux_n(fl, Xg, (0.0, 1.0))[:, 0]
+    assert torch.allclose(fx, (K * g[:, 0]).detach(), rtol=1e-13)
+    assert torch.allclose(fy, (K * g[:, 1]).detach(), rtol=1e-13)
+    fl3, Xg3 = _autograd_fields([Tf, _tk(X)[1]], X)
+    flh, Xgh = _autograd_fields([Tf], X)
+    assert torch.allclose(opde.heat_inv_residual(fl3, Xg3), opde.heat_residual(flh, Xgh), rtol=1e-12, atol=1e-11)
+
+
+def test_heat_inv_c5_targets_are_the_paper_fields():
+    p = make_config("C5", scale=0.05)
+    for s in p.subdomains:
+        x = s.x_u
+        np.testing.assert_allclose(s.u_target[:, 0], 20.0 * np.exp(-0.1 * x[:, 1]), rtol=1e-6)
+        np.testing.assert_allclose(s.u_target[:, 1], 20.0 + np.exp(0.1 * x[:, 1]) * np.sin(0.5 * x[:, 0]),
+                                   rtol=1e-6)
+        assert np.all(s.u_mask[:, 0] == 1.0)           # T data everywhere (interior + boundary)
