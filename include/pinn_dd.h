@@ -70,8 +70,10 @@ typedef enum {
    x2-normal edges (XPINN, Eq. 6). */
 enum { PINN_DD_METHOD_PINN = 0, PINN_DD_METHOD_CPINN = 1, PINN_DD_METHOD_XPINN = 2, PINN_DD_METHOD_HYBRID = 3 };
 /* P:313-316 Burgers; P:823-829 heat (K known; POISSON = K==1 with u* = sin(pi x) sin(pi y));
-   P:415-417 steady incompressible NS (outputs u, v, p). */
-enum { PINN_DD_PDE_BURGERS = 0, PINN_DD_PDE_POISSON = 1, PINN_DD_PDE_HEAT = 2, PINN_DD_PDE_NS = 3 };
+   P:415-417 steady incompressible NS (outputs u, v, p); P:821-871 inverse heat conduction
+   HEAT_INV: one net per region with outputs (T, K), F = div(K grad T) - f, f = 4 exp(-0.1 y). */
+enum { PINN_DD_PDE_BURGERS = 0, PINN_DD_PDE_POISSON = 1, PINN_DD_PDE_HEAT = 2, PINN_DD_PDE_NS = 3,
+       PINN_DD_PDE_HEAT_INV = 4 };
 enum { PINN_DD_ACT_TANH = 0, PINN_DD_ACT_SIN = 1, PINN_DD_ACT_COS = 2 };
 
 /* flags */
@@ -93,9 +95,9 @@ typedef struct {
   /* ---- problem ---------------------------------- */
   int32_t method;      /* PINN_DD_METHOD_*                                   */
   int32_t pde;         /* PINN_DD_PDE_*                                      */
-  int32_t activation;  /* PINN_DD_ACT_*                                      */
+  int32_t activation;  /* PINN_DD_ACT_* (all subdomains unless sub_activation) */
   int32_t d_in;        /* must be 2                                          */
-  int32_t d_out;       /* 1, or 3 for NS                                     */
+  int32_t d_out;       /* 1; 3 for NS (u, v, p); 2 for HEAT_INV (T, K)       */
   int32_t width;       /* N_k of every hidden layer                          */
   int32_t n_hidden;    /* L-1 hidden layers                                  */
   float slope_n;       /* n of the adaptive slope n a^k (n = 10)       */
@@ -130,6 +132,11 @@ typedef struct {
                                 MSE_u instead of the local counts: a rank holding a shard of
                                 a subdomain's points then produces exactly its additive share
                                 of J and dJ/dTheta (sum over ranks = the full-data values). */
+  /* ---- per-subdomain activation (host, nullable) ---------------------- */
+  const int32_t* sub_activation; /* [n_sub] PINN_DD_ACT_* of each subdomain's net (Table 3,
+                                P:862-866: tanh / sin / cos per region); NULL = `activation`
+                                everywhere.  Mixed values need a network shape compiled with
+                                per-subdomain activations (else PINN_DD_EUNSUPPORTED). */
 } pinn_dd_desc;
 
 /* Number of packed parameters of one network [d_in, width x n_hidden, d_out]:

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("PINN_DD_LIB", os.path.join(_HERE, "libpinn_dd.so"))
 
 OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, ENONFINITE, EPROTOCOL = range(7)
 METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2, "hybrid": 3}
-PDES = {"burgers": 0, "poisson": 1, "heat": 2, "ns": 3}
+PDES = {"burgers": 0, "poisson": 1, "heat": 2, "ns": 3, "heat_inv": 4}
 ACTS = {"tanh": 0, "sin": 1, "cos": 2}
 FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING = 1, 2, 4
 
@@ -62,6 +62,7 @@ class Desc(C.Structure):
         ("coords", C.c_void_p), ("target", C.c_void_p), ("mask", C.c_void_p), ("init_params", C.c_void_p),
         ("stream", C.c_void_p), ("flags", C.c_int32),
         ("sub_norm_counts", C.POINTER(C.c_int32)),
+        ("sub_activation", C.POINTER(C.c_int32)),
     ]
 
 
@@ -240,6 +241,9 @@ def make_desc(prob, t: PointTable, dev_ptrs: Dict[str, int], stream: int = 0, fl
     d.flags = flags
     if norm_counts is not None:
         d.sub_norm_counts = ptr(np.asarray(norm_counts, dtype=np.int32).reshape(-1), C.c_int32)
+    acts = [ACTS[prob.act(q)] for q in t.local]
+    if any(a != d.activation for a in acts):
+        d.sub_activation = ptr(np.asarray(acts, dtype=np.int32), C.c_int32)
     return d, keep
 
 

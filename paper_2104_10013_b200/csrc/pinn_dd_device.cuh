@@ -114,16 +114,24 @@ struct KCfg {
 
 // ----------------------------------------------------------------------------
 // activations sigma, sigma', sigma'', sigma''' (ACT: 0 tanh, 1 sin, 2 cos)
+// kActMixed: the activation is the runtime argument `act`, one per subdomain
+// (Table 3) -- uniform per chunk, so the branch never diverges.
 // ----------------------------------------------------------------------------
+constexpr int kActMixed = 3;
 template <int ACT>
-__device__ __forceinline__ void act_derivs(float u, float& s0, float& s1, float& s2, float& s3) {
-  if (ACT == 0) {
+__device__ __forceinline__ int act_sel(int act) {
+  return ACT == kActMixed ? act : ACT;
+}
+template <int ACT>
+__device__ __forceinline__ void act_derivs(float u, float& s0, float& s1, float& s2, float& s3, int act = ACT) {
+  const int A = act_sel<ACT>(act);
+  if (A == 0) {
     float t = tanhf(u);
     s0 = t;
     s1 = 1.0f - t * t;
     s2 = -2.0f * t * s1;
     s3 = s1 * (6.0f * t * t - 2.0f);
-  } else if (ACT == 1) {
+  } else if (A == 1) {
     float sn, cs;
     sincosf(u, &sn, &cs);
     s0 = sn; s1 = cs; s2 = -sn; s3 = -cs;
@@ -139,28 +147,29 @@ __device__ __forceinline__ void act_derivs(float u, float& s0, float& s1, float&
 // polynomial in t = tanh(s z), so the stash keeps (t, g1, g2, L) and the
 // reverse pass evaluates no transcendental; sin / cos keep z itself.
 template <int ACT>
-__device__ __forceinline__ float stash_x(float zx, float s) {
-  return ACT == 0 ? tanhf(s * zx) : zx;
+__device__ __forceinline__ float stash_x(float zx, float s, int act = ACT) {
+  return act_sel<ACT>(act) == 0 ? tanhf(s * zx) : zx;
 }
 template <int ACT>
-__device__ __forceinline__ void derivs_from_stash(float x, float s, float& s0, float& s1, float& s2, float& s3) {
-  if (ACT == 0) {
+__device__ __forceinline__ void derivs_from_stash(float x, float s, float& s0, float& s1, float& s2, float& s3,
+                                                  int act = ACT) {
+  if (act_sel<ACT>(act) == 0) {
     const float t = x;
     s0 = t;
     s1 = 1.0f - t * t;
     s2 = -2.0f * t * s1;
     s3 = s1 * (6.0f * t * t - 2.0f);
   } else {
-    act_derivs<ACT>(s * x, s0, s1, s2, s3);
+    act_derivs<ACT>(s * x, s0, s1, s2, s3, act);
   }
 }
 
 // forward jet map of one neuron from its stash form (x, g1, g2, L):
 // h = (sigma, sigma' s g1, sigma' s g2, sigma'' s^2 Q + sigma' s L)
 template <int ACT>
-__device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2) {
+__device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2, int act = ACT) {
   float s0, s1, s2, s3;
-  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3);
+  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3, act);
   const float Q = m1 * z.y * z.y + m2 * z.z * z.z;
   const float ss = s1 * s;
   float4 h;
@@ -177,9 +186,9 @@ __device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2)
 // s_k b^k, so a_k dJ/da_k = <W^k, dJ/dW^k> + <b^k, dJ/db^k> exactly; K5
 // evaluates that identity once per step.
 template <int ACT>
-__device__ __forceinline__ float4 act_bwd(float4 z, float4 hb, float s, float m1, float m2) {
+__device__ __forceinline__ float4 act_bwd(float4 z, float4 hb, float s, float m1, float m2, int act = ACT) {
   float s0, s1, s2, s3;
-  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3);
+  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3, act);
   const float Q = m1 * z.y * z.y + m2 * z.z * z.z;
   const float zb = hb.x * s1 + s * s2 * (hb.y * z.y + hb.z * z.z) + hb.w * (s3 * s * s * Q + s2 * s * z.w);
   const float g1 = hb.y * s1 + 2.0f * m1 * hb.w * s2 * s * z.y;
@@ -262,7 +271,7 @@ struct Stash {
 // pointwise operators.  U[o] = (u, d1 u, d2 u, Delta_S u) of output o.
 // r[e] and dr[e][o][c] = d r_e / d U[o].c
 // ----------------------------------------------------------------------------
-constexpr int PDE_BURGERS = 0, PDE_POISSON = 1, PDE_HEAT = 2, PDE_NS = 3;
+constexpr int PDE_BURGERS = 0, PDE_POISSON = 1, PDE_HEAT = 2, PDE_NS = 3, PDE_HEAT_INV = 4;
 
 struct PdeConst {
   int pde;
@@ -309,6 +318,17 @@ __device__ __forceinline__ int pde_residual(const PdeConst& pc, const float4* U,
     r[0] = K * u.w + Kx * u.y + Ky * u.z - f;
     dr[0][0][1] = Kx; dr[0][0][2] = Ky; dr[0][0][3] = K;
     return 1;
+  } else if (pc.pde == PDE_HEAT_INV) {
+    // inverse heat (K unknown): outputs (T, K) of one net,
+    // F = K Delta T + K_x T_x + K_y T_y - f, f = 4 exp(-0.1 y) (reading Z17b)
+    if constexpr (DO == 2) {
+      const float4 T = U[0], K = U[1];
+      const float f = 4.0f * __expf(-0.1f * y);
+      r[0] = K.x * T.w + K.y * T.y + K.z * T.z - f;
+      dr[0][0][1] = K.y; dr[0][0][2] = K.z; dr[0][0][3] = K.x;
+      dr[0][1][0] = T.w; dr[0][1][1] = T.y; dr[0][1][2] = T.z;
+    }
+    return 1;
   } else {
     // steady incompressible NS, outputs (u, v, p)
     if constexpr (DO == 3) {
@@ -350,6 +370,16 @@ __device__ __forceinline__ int pde_flux(const PdeConst& pc, const float4* U, flo
     dr[0][0][1] = K * n1;
     dr[0][0][2] = K * n2;
     return 1;
+  } else if (pc.pde == PDE_HEAT_INV) {
+    // K grad T . n with K the net's second output
+    if constexpr (DO == 2) {
+      const float4 T = U[0], K = U[1];
+      const float gn = T.y * n1 + T.z * n2;
+      r[0] = K.x * gn;
+      dr[0][0][1] = K.x * n1; dr[0][0][2] = K.x * n2;
+      dr[0][1][0] = gn;
+    }
+    return 1;
   } else {
     if constexpr (DO == 3) {
       const float4 u = U[0], v = U[1], p = U[2];
@@ -386,6 +416,7 @@ struct KArgs {
   const int32_t* ptwin;     // payload row of the twin (interface points)
   const float2* seg_normal; // [n_seg]
   const float* params;      // internal [n_sub][PSTRIDE]
+  const int32_t* sub_act;   // [n_sub] activation per subdomain (read only by kActMixed instances)
   const float4* sub_w;      // [n_sub] (w_u, w_f, w_i, w_if)
   const Chunk* chunks;
   int n_chunks;

@@ -35,7 +35,8 @@ struct Ops {
   size_t smem;     // dynamic smem of the fused kernel
   void (*k1)(const KArgs&, int grid, size_t smem, cudaStream_t);
   void (*k2)(const KArgs&, int grid, size_t smem, cudaStream_t);
-  void (*pred)(const float*, int, float, const float*, const int32_t*, int64_t, float*, cudaStream_t);
+  void (*pred)(const float*, int, float, const float*, const int32_t*, int64_t, float*, const int32_t*,
+               cudaStream_t);
   void (*packmap)(std::vector<int32_t>&);
   void (*slopetab)(RArgs&);
   cudaError_t (*setattr)(size_t);
@@ -53,10 +54,11 @@ struct Inst {
     k_fused<N, NH, DO, ACT, 1><<<grid, kThreads, sm, s>>>(a);
   }
   static void pred(const float* params, int pstride, float sn, const float* pts, const int32_t* own, int64_t n,
-                   float* out, cudaStream_t s) {
+                   float* out, const int32_t* sub_act, cudaStream_t s) {
     const int bs = 128;
     const int64_t g = (n + bs - 1) / bs;
-    if (g > 0) k_predict<N, NH, DO, ACT><<<unsigned(g), bs, 0, s>>>(params, pstride, sn, pts, own, n, out);
+    if (g > 0)
+      k_predict<N, NH, DO, ACT><<<unsigned(g), bs, 0, s>>>(params, pstride, sn, pts, own, n, out, sub_act);
   }
   // packed index -> internal offset (layer-major W, b, a)
   static void packmap(std::vector<int32_t>& m) {
@@ -90,10 +92,12 @@ struct Inst {
   }
 };
 
-// The shapes of BASELINE.json configs C1-C4 (tanh): 3x20, 5x20, 6x40, 5x80 (D_o = 3).
+// The shapes of BASELINE.json configs C1-C4 (tanh): 3x20, 5x20, 6x40, 5x80 (D_o = 3);
+// C5 (inverse heat, outputs (T, K)): 3x80 with tanh / sin / cos per region (Table 3).
 const Ops* find_ops(int N, int NH, int DO, int ACT) {
   static const Ops table[] = {
       Inst<20, 3, 1, 0>::ops(), Inst<20, 5, 1, 0>::ops(), Inst<40, 6, 1, 0>::ops(), Inst<80, 5, 3, 0>::ops(),
+      Inst<80, 3, 2, kActMixed>::ops(),
   };
   for (const Ops& o : table)
     if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT) return &o;
@@ -105,7 +109,7 @@ const Ops* find_ops(int N, int NH, int DO, int ACT) {
 struct pinn_dd {
   // copied descriptor + owned host arrays
   pinn_dd_desc d;
-  std::vector<int32_t> sub_off, n_res, n_data, seg_off, seg_n, norm_counts;
+  std::vector<int32_t> sub_off, n_res, n_data, seg_off, seg_n, norm_counts, act;
   std::vector<int64_t> seg_twin;
   std::vector<float> seg_normal;
   std::vector<pinn_dd_hparams> hp;
@@ -119,7 +123,7 @@ struct pinn_dd {
   float *partial = nullptr, *partial_loss = nullptr, *payload = nullptr, *loss = nullptr;
   float *pinv = nullptr, *gstash = nullptr, *scratch = nullptr;
   int32_t *pinfo = nullptr, *ptwin = nullptr, *sub_chunk = nullptr, *tstep = nullptr, *done = nullptr;
-  int32_t *flag = nullptr, *packmap = nullptr;
+  int32_t *flag = nullptr, *packmap = nullptr, *sub_act = nullptr;
   float2* segn = nullptr;
   float4 *sub_w = nullptr, *sub_adam = nullptr;
   Chunk *chunks1 = nullptr, *chunks2 = nullptr;
@@ -176,7 +180,7 @@ struct Carve {
 };
 
 struct Layout {
-  size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, ch1, ch2, subch,
+  size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ch2, subch,
       tstep, done, flag, loss, packmap, gstash, total;
 };
 
@@ -185,13 +189,26 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   if (!d) return fail(h, PINN_DD_EINVAL, "desc is NULL");
   if (d->d_in != 2) return fail(h, PINN_DD_EINVAL, "d_in must be 2 (got %d)", d->d_in);
   if (d->method < 0 || d->method > 3) return fail(h, PINN_DD_EINVAL, "bad method %d", d->method);
-  if (d->pde < 0 || d->pde > 3) return fail(h, PINN_DD_EINVAL, "bad pde %d", d->pde);
-  const int want_do = d->pde == PINN_DD_PDE_NS ? 3 : 1;
+  if (d->pde < 0 || d->pde > 4) return fail(h, PINN_DD_EINVAL, "bad pde %d", d->pde);
+  const int want_do = d->pde == PINN_DD_PDE_NS ? 3 : (d->pde == PINN_DD_PDE_HEAT_INV ? 2 : 1);
   if (d->d_out != want_do) return fail(h, PINN_DD_EINVAL, "d_out %d does not match pde %d", d->d_out, d->pde);
-  const Ops* ops = find_ops(d->width, d->n_hidden, d->d_out, d->activation);
+  if (d->activation < 0 || d->activation > 2) return fail(h, PINN_DD_EINVAL, "bad activation %d", d->activation);
+  bool mixed = false;
+  if (d->sub_activation) {
+    if (d->n_sub < 1) return fail(h, PINN_DD_EINVAL, "n_sub must be >= 1");
+    for (int q = 0; q < d->n_sub; ++q) {
+      if (d->sub_activation[q] < 0 || d->sub_activation[q] > 2)
+        return fail(h, PINN_DD_EINVAL, "subdomain %d: bad activation %d", q, d->sub_activation[q]);
+      mixed |= d->sub_activation[q] != d->sub_activation[0];
+    }
+  }
+  const int act0 = d->sub_activation ? d->sub_activation[0] : d->activation;
+  // one compiled activation if uniform, else the per-subdomain (kActMixed) instance
+  const Ops* ops = mixed ? nullptr : find_ops(d->width, d->n_hidden, d->d_out, act0);
+  if (!ops) ops = find_ops(d->width, d->n_hidden, d->d_out, kActMixed);
   if (!ops)
-    return fail(h, PINN_DD_EUNSUPPORTED, "network [2, %dx%d, %d] activation %d not compiled in", d->width,
-                d->n_hidden, d->d_out, d->activation);
+    return fail(h, PINN_DD_EUNSUPPORTED, "network [2, %dx%d, %d] activation %d%s not compiled in", d->width,
+                d->n_hidden, d->d_out, act0, mixed ? " (mixed per subdomain)" : "");
   if (d->n_sub < 1) return fail(h, PINN_DD_EINVAL, "n_sub must be >= 1");
   if (!d->sub_point_offset || !d->sub_n_res || !d->sub_n_data || !d->sub_seg_offset || !d->sub_hparams)
     return fail(h, PINN_DD_EINVAL, "subdomain arrays must not be NULL");
@@ -274,6 +291,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->ptwin = c.take<int32_t>(npt + 1);
   L->segn = c.take<float2>(size_t(d->n_seg) + 1);
   L->subw = c.take<float4>(ns);
+  L->subact = c.take<int32_t>(ns);
   L->suba = c.take<float4>(ns);
   L->ch1 = c.take<Chunk>(size_t(n1));
   L->ch2 = c.take<Chunk>(size_t(n2) + 1);
@@ -319,6 +337,7 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.seg_normal = h->segn;
   a.params = h->params;
   a.sub_w = h->sub_w;
+  a.sub_act = h->sub_act;
   a.chunks = payload_tiles ? h->chunks2 : h->chunks1;
   a.n_chunks = payload_tiles ? h->n_chunks2 : h->n_chunks1;
   a.n_points = d.n_points;
@@ -485,6 +504,11 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->d.seg_twin = h->seg_twin.data();
   h->d.seg_normal = h->seg_normal.data();
   h->d.sub_norm_counts = d->sub_norm_counts ? h->norm_counts.data() : nullptr;
+  if (d->sub_activation)
+    h->act.assign(d->sub_activation, d->sub_activation + ns);
+  else
+    h->act.assign(ns, d->activation);
+  h->d.sub_activation = h->act.data();
   h->stream = static_cast<cudaStream_t>(d->stream);
 
   char* base = static_cast<char*>(ws);
@@ -501,6 +525,7 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->ptwin = reinterpret_cast<int32_t*>(base + L.ptwin);
   h->segn = reinterpret_cast<float2*>(base + L.segn);
   h->sub_w = reinterpret_cast<float4*>(base + L.subw);
+  h->sub_act = reinterpret_cast<int32_t*>(base + L.subact);
   h->sub_adam = reinterpret_cast<float4*>(base + L.suba);
   h->chunks1 = reinterpret_cast<Chunk*>(base + L.ch1);
   h->chunks2 = reinterpret_cast<Chunk*>(base + L.ch2);
@@ -604,6 +629,7 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   if (d->n_seg > 0)
     CKC(cudaMemcpyAsync(h->segn, h->seg_normal.data(), h->seg_normal.size() * 4, cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->sub_w, subw.data(), subw.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->sub_act, h->act.data(), h->act.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->sub_adam, suba.data(), suba.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->chunks1, c1.data(), c1.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
   if (!c2.empty())
@@ -743,7 +769,7 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
 pinn_dd_status pinn_dd_predict(pinn_dd* h, const float* pts, const int32_t* owners, int64_t n, float* out) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
   if (n < 0 || (n > 0 && (!pts || !owners || !out))) return fail(h, PINN_DD_EINVAL, "bad predict arguments");
-  h->ops->pred(h->params, h->pstride, h->d.slope_n, pts, owners, n, out, h->stream);
+  h->ops->pred(h->params, h->pstride, h->d.slope_n, pts, owners, n, out, h->sub_act, h->stream);
   ++h->launches;
   CK(h, cudaGetLastError());
   return PINN_DD_OK;

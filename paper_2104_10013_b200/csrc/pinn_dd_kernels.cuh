@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       cur_sub = ch.sub;
     }
     const float4 lw = a.sub_w[ch.sub];
+    const int act = ACT == kActMixed ? a.sub_act[ch.sub] : ACT;   // uniform per chunk
     float* Pc = a.partial + size_t(c) * a.pstride;
     float* A = DSM ? sAcc : Pc;   // gradient accumulator of this chunk
     if constexpr (MODE == 0 && DSM) {
@@ -358,10 +359,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         }
         const float s = sSl[0];
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s);
+        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s, act);
         if constexpr (MODE == 0) st.store(0, z);
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
+        for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2, act);
       }
       cta_sync();
 #pragma unroll 1
@@ -371,10 +372,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         gemm_fwd<N, NH, DO>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
         const float s = sSl[k - 1];
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s);
+        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s, act);
         if constexpr (MODE == 0) st.store(k - 1, z);
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2);
+        for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2, act);
         cta_sync();
       }
       const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
@@ -533,12 +534,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           st.load(NH - 1, z);
           const float s = sSl[NH - 1];
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2));
+          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, act));
           if (NH >= 2) {
             st.load(NH - 2, z);
             const float s2 = sSl[NH - 2];
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2));
+            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2, act));
           }
         }
         float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
@@ -559,13 +560,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           st.load(k - 2, z);
           const float s = sSl[k - 2];
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2));
+          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, act));
           const bool more = (k - 1 >= 2);
           if (more) {
             st.load(k - 3, z);
             const float s2 = sSl[k - 3];
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2));
+            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2, act));
           }
           cta_sync();
 #pragma unroll
@@ -759,7 +760,7 @@ __global__ void k_scatter(const float* src, const int32_t* map, int n, int pstri
 // ----------------------------------------------------------------------------
 template <int N, int NH, int DO, int ACT>
 __global__ void k_predict(const float* params, int pstride, float slope_n, const float* pts, const int32_t* owners,
-                          int64_t n, float* out) {
+                          int64_t n, float* out, const int32_t* sub_act) {
   using LY = Lay<N, NH, DO>;
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -772,13 +773,14 @@ __global__ void k_predict(const float* params, int pstride, float slope_n, const
     const int q = owners[p * 4 + k];
     if (q < 0) continue;
     ++S;
+    const int act = ACT == kActMixed ? sub_act[q] : ACT;
     const float* G = params + size_t(q) * pstride;
     float h[N], g[N];
     float s = slope_n * G[LY::offA(1)];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       float s0, s1, s2, s3;
-      act_derivs<ACT>(s * (G[2 * j] * x + G[2 * j + 1] * y + G[LY::offB(1) + j]), s0, s1, s2, s3);
+      act_derivs<ACT>(s * (G[2 * j] * x + G[2 * j + 1] * y + G[LY::offB(1) + j]), s0, s1, s2, s3, act);
       h[j] = s0;
     }
     for (int l = 2; l <= NH; ++l) {
@@ -794,7 +796,7 @@ __global__ void k_predict(const float* params, int pstride, float slope_n, const
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         float s0, s1, s2, s3;
-        act_derivs<ACT>(s * g[j], s0, s1, s2, s3);
+        act_derivs<ACT>(s * g[j], s0, s1, s2, s3, act);
         h[j] = s0;
       }
     }

@@ -109,6 +109,10 @@ CASES = [
     ("C4", dict(method="xpinn", n_f=150, n_i=20, n_u=16)),
     ("C4", dict(method="cpinn", n_f=150, n_i=20, n_u=16)),
     ("C3", dict(method="hybrid", gpus=8, n_f=300, n_i=30, n_u=40)),   # P:948 cPINN-x + XPINN-t
+    # C5 inverse heat: 10 Voronoi regions, outputs (T, K), Table 3 tanh/sin/cos per region
+    ("C5", dict(scale=0.02, n_i=24, n_u=40)),                                         # [10]
+    ("C5", dict(method="cpinn", scale=0.02, n_i=24, n_u=40)),                         # oblique K grad T . n
+    ("C5", dict(scale=0.02, n_i=24, n_u=40, activations=["cos"] * 10)),              # uniform non-tanh
 ]
 
 
@@ -118,7 +122,7 @@ def test_loss_grad_parity(cfg, kw):
     run_parity(prob, f"{cfg}{kw}")
 
 
-@pytest.mark.parametrize("cfg,kw", [CASES[1], CASES[3], CASES[5], CASES[7]])
+@pytest.mark.parametrize("cfg,kw", [CASES[1], CASES[3], CASES[5], CASES[7], CASES[10]])
 def test_loss_grad_parity_perturbed(cfg, kw):
     """Away from n a = 1 and b = 0 (exercises the bias and slope paths)."""
     prob = perturb_params(make_config(cfg, **kw), scale=0.2)
@@ -130,7 +134,8 @@ def test_pinn_method_single_subdomain():
     run_parity(prob, "pinn")
 
 
-@pytest.mark.parametrize("cfg,kw", [CASES[3], CASES[2], CASES[7], CASES[8], CASES[0], CASES[9]])
+@pytest.mark.parametrize("cfg,kw", [CASES[3], CASES[2], CASES[7], CASES[8], CASES[0], CASES[9], CASES[10],
+                                    CASES[11]])
 def test_payload_parity(cfg, kw):
     """K2: u(x_I) and f.n / F(x_I) of every local interface point."""
     prob = make_config(cfg, **kw)
@@ -278,6 +283,44 @@ def test_predict_stitching():
     ref = OL.stitch(prob, OL.init_state(prob).thetas, X.astype(np.float64)).numpy()
     np.testing.assert_allclose(out.cpu().numpy().T, ref, rtol=1e-5, atol=1e-6)
     m.close()
+
+
+def test_predict_stitching_c5_voronoi():
+    """Eq. (4) on the C5 map with per-region activations: owners = nearest
+    seed(s) inside the polygon (1/S on interfaces), 0 outside."""
+    from pinn_inputs import voronoi as vor
+    prob = make_config("C5", scale=0.02, n_i=10, n_u=20)
+    m = _handle(prob)
+    rng = np.random.default_rng(2)
+    X = rng.uniform(prob.domain_lo, prob.domain_hi, size=(400, 2))
+    X = np.concatenate([X, prob.edges[0].pts[:3], prob.edges[-1].pts[:2]]).astype(np.float32)
+    seeds = prob.meta["seeds"]
+    d = np.linalg.norm(X[:, None, :].astype(np.float64) - seeds[None], axis=2)
+    ins = vor.inside(prob.meta["polygon"], X.astype(np.float64))
+    owners = np.full((len(X), 4), -1, np.int32)
+    own = []
+    for i in range(len(X)):
+        o = [] if not ins[i] else list(np.flatnonzero(d[i] <= d[i].min() + 1e-5))
+        owners[i, :len(o)] = o
+        own.append(o)
+    out = m.predict(torch.tensor(X.T.copy(), device="cuda:0"), torch.tensor(owners, device="cuda:0"))
+    th = OL.init_state(prob).thetas
+    from oracle import net as onet
+    ref = np.zeros((len(X), 2))
+    Xt = torch.tensor(X.astype(np.float64))
+    for q in range(prob.n_sub):
+        w = np.array([1.0 / len(o) if q in o else 0.0 for o in own])
+        if w.any():
+            ref += w[:, None] * onet.forward(th[q], prob.sizes, Xt, prob.act(q), prob.slope_n).numpy()
+    assert sum(len(o) == 2 for o in own) >= 5
+    np.testing.assert_allclose(out.cpu().numpy().T, ref, rtol=1e-5, atol=1e-5)
+    m.close()
+
+
+def test_full_size_c5_parity():
+    """BASELINE configs[4] (C5) at full size: 10 regions, Table 3 residual
+    counts (36,800 points), per-region activations: loss and gradients."""
+    run_parity(make_config("C5"), "full C5")
 
 
 def test_full_size_c2_parity():
