@@ -59,6 +59,17 @@ def flops_per_point(width: int, n_hidden: int, d_out: int, C: int = 4, d: int = 
     return fwd + 2 * lin + (6 * d + 25) * N * NH
 
 
+def lpt_owner(loads, world):
+    """Longest-processing-time placement: heaviest unit to the least-loaded GPU."""
+    owner = [0] * len(loads)
+    tot = [0] * world
+    for q in sorted(range(len(loads)), key=lambda i: (-loads[i], i)):
+        g = min(range(world), key=lambda r: (tot[r], r))
+        owner[q] = g
+        tot[g] += loads[q]
+    return owner
+
+
 def algorithmic_flops(prob, local):
     """K1 (loss+grad) FLOPs of one step for the local subdomains, and K2 (payload)."""
     N, NH, DO = prob.width, prob.n_hidden, prob.d_out
@@ -181,7 +192,8 @@ def run_reference(args):
     import torch
     from pinn_inputs import make_config
     from oracle import loss as OL
-    prob = make_config("C2", method=args.method, weak=args.gpus)
+    prob = (make_config("C5", method=args.method) if args.workload == "c5"
+            else make_config("C2", method=args.method, weak=args.gpus))
     st = OL.init_state(prob)
     for w in range(args.warmup):
         oracle_sample_step(prob, st, w % prob.n_sub)
@@ -195,8 +207,8 @@ def run_reference(args):
               f"with its neighbours' payloads; {args.steps} steps, {pts} pts, {dt:.1f} s")
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(1, args.steps), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
+            "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{prob.name} {prob.method} (oracle sample)", "subdomains": prob.n_sub,
                        "net": f"2-{prob.width}x{prob.n_hidden}-{prob.d_out} tanh"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
@@ -238,6 +250,14 @@ def run_ours(args):
         dp = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=FLAG_TIMING)
         h = dp.h
         h_prob, local = h.prob, [0]
+    elif args.workload == "c5":
+        # C5 inverse heat: the fixed 10-region map,
+        # regions placed on GPUs by LPT on their point counts (strong scaling)
+        prob = make_config("C5", method=args.method)
+        owner = lpt_owner([prob.n_points(q) for q in range(prob.n_sub)], world)
+        local = [q for q in range(prob.n_sub) if owner[q] == rank]
+        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING)
+        h_prob = prob
     else:
         prob = make_config("C2", method=args.method, weak=world)
         owner = [s.ix // 4 for s in prob.subdomains]          # one 4x4 block per GPU
@@ -327,23 +347,28 @@ def run_ours(args):
             traffic = None
 
     if rank == 0:
-        base = (cpu_baseline(make_config("C2", method=args.method)) if (world == 1 and not args.no_cpu
-                                                                       and args.method != "dp") else None)
+        base_prob = make_config("C5", method=args.method) if args.workload == "c5" else \
+            make_config("C2", method=args.method)
+        base = (cpu_baseline(base_prob) if (world == 1 and not args.no_cpu and args.method != "dp") else None)
+        acts = sorted({prob.act(q) for q in local})
+        kname = (f"K1 k_fused<{prob.width},{prob.n_hidden},{prob.d_out},"
+                 f"{'mixed' if len(acts) > 1 else acts[0]}> (fused fwd jets + loss + reverse)")
         share = kt[1] / max(1e-9, sum(kt[:3]))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
             "iters_per_s": 1e3 * args.steps / t_max,
             "config": {"workload": f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}",
                        "subdomains": prob.n_sub,
                        "subdomains_per_gpu": len(local), "points_per_step": int(pts_all.item()),
-                       "net": f"2-{prob.width}x{prob.n_hidden}-{prob.d_out} tanh, adaptive slope n=10",
+                       "net": f"2-{prob.width}x{prob.n_hidden}-{prob.d_out} {'/'.join(acts)}, adaptive slope n=10",
                        "parallelism": f"domain decomposition, {len(local)} subdomains/GPU, P2P exchange",
                        "l2": "flushed (256 MiB write) between timed steps"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                          "frac": achieved / peak_fp32, "traffic": traffic,
-                         "kernel": "K1 k_fused<40,6,1,tanh> (fused fwd jets + loss + reverse)",
+                         "kernel": kname,
                          "k1_ms_per_launch": k1_ms, "k1_gflop_per_launch": k1_flops / 1e9,
                          "k1_share_of_step": share,
                          "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md clocks.max.sm)"},
@@ -368,10 +393,17 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--method", choices=["cpinn", "xpinn", "hybrid", "dp"], default="cpinn",
-                    help="dp = data-parallel vanilla PINN comparator (Table 2)")
+    ap.add_argument("--method", choices=["cpinn", "xpinn", "hybrid", "dp"], default=None,
+                    help="default cpinn for c2, xpinn for c5; dp = data-parallel vanilla PINN comparator "
+                         "(Table 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--workload", choices=["c2", "c5"], default="c2",
+                    help="c2: BASELINE configs[1] (default, the headline); c5: inverse heat map (configs[4])")
     args = ap.parse_args()
+    if args.method is None:
+        args.method = "xpinn" if args.workload == "c5" else "cpinn"
+    if args.workload == "c5" and args.method == "dp":
+        raise SystemExit("--method dp is the C2 data-parallel comparator")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
