@@ -227,18 +227,32 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
       }
     }
   }
+}
+
+// second half of gemm_dw for S > 1: sum the S point-split partials in fixed
+// order into the accumulator.  Called after the CTA barrier that follows
+// gemm_bwd, so it needs no barrier of its own and its shared-memory latency
+// overlaps the activation-buffer stores that follow.
+template <int N, int NH, int DO, bool DWS>
+__device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool first, const float* sDw) {
+  using C = KCfg<N, NH, DO>;
+  constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
+  constexpr int DBOFF = S * NBLK * JB * IB;
   if constexpr (S > 1) {
-    cta_sync();
+    const int tid = threadIdx.x;
     for (int e = tid; e < NBLK * JB; e += kThreads) {   // (block, row) items; IB columns each
       const int r = e / JB, jj = e - (e / JB) * JB;
       const int jb = r % NJ, ib = r / NJ;
+      const float* src = sDw + r * JB * IB + jj * IB;
+      float v[IB];
 #pragma unroll
-      for (int ii = 0; ii < IB; ++ii) {
-        float v = 0.0f;
+      for (int ii = 0; ii < IB; ++ii) v[ii] = src[ii];
 #pragma unroll
-        for (int s = 0; s < S; ++s) v += sDw[(s * NBLK + r) * JB * IB + jj * IB + ii];
-        acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v, first);
-      }
+      for (int s = 1; s < S; ++s)
+#pragma unroll
+        for (int ii = 0; ii < IB; ++ii) v[ii] += src[s * NBLK * JB * IB + ii];
+#pragma unroll
+      for (int ii = 0; ii < IB; ++ii) acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v[ii], first);
     }
     for (int e = tid; e < NJ * JB; e += kThreads) {
       const int jb = e / JB, jj = e % JB;
@@ -554,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 #pragma unroll 1
         for (int k = NH; k >= 2; --k) {
           // dW^k, db^k
-          gemm_dw<N, NH, DO, DSM>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);
+          gemm_dw<N, NH, DO, DSM>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
           // adjoint of H^{k-1}, then of Z^{k-1}
           gemm_bwd<N, NH, DO>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
           st.load(k - 2, z);
@@ -569,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
             for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2, act));
           }
           cta_sync();
+          gemm_dw_reduce<N, NH, DO, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
             bufZ[(j0 + jj) * C::PSTR + pg] = f4(hb, jj);
