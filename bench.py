@@ -171,6 +171,18 @@ def cpu_baseline(prob, budget_s: float = 20.0):
     import torch
     from oracle import loss as OL
     st = OL.init_state(prob)
+    if prob.n_points() > 300_000:
+        # too large for full oracle steps within the budget (C4: 1M points): time
+        # loss+grad+Adam of single subdomains (with their neighbours' payloads) instead
+        t0 = time.perf_counter()
+        pts = k = 0
+        while k == 0 or time.perf_counter() - t0 < budget_s:
+            pts += oracle_sample_step(prob, st, k % prob.n_sub)
+            k += 1
+        dt = time.perf_counter() - t0
+        return {"value": pts / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
+                "sample": f"{k} single-subdomain FP64 oracle step(s) of {prob.name} {prob.method} "
+                          f"({pts} pts), {dt:.1f} s"}
     t0 = time.perf_counter()
     steps = 0
     while True:
@@ -192,8 +204,9 @@ def run_reference(args):
     import torch
     from pinn_inputs import make_config
     from oracle import loss as OL
-    prob = (make_config("C5", method=args.method) if args.workload == "c5"
-            else make_config("C2", method=args.method, weak=args.gpus))
+    prob = (make_config("C2", method=args.method, weak=args.gpus) if args.workload == "c2"
+            else make_config(args.workload.upper(), method=args.method,
+                             **({"gpus": 8} if args.workload == "c3" else {})))
     st = OL.init_state(prob)
     for w in range(args.warmup):
         oracle_sample_step(prob, st, w % prob.n_sub)
@@ -207,7 +220,7 @@ def run_reference(args):
               f"with its neighbours' payloads; {args.steps} steps, {pts} pts, {dt:.1f} s")
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(1, args.steps), "higher_is_better": True,
-            "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{prob.name} {prob.method} (oracle sample)", "subdomains": prob.n_sub,
                        "net": f"2-{prob.width}x{prob.n_hidden}-{prob.d_out} tanh"},
@@ -250,10 +263,13 @@ def run_ours(args):
         dp = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=FLAG_TIMING)
         h = dp.h
         h_prob, local = h.prob, [0]
-    elif args.workload == "c5":
-        # C5 inverse heat: the fixed 10-region map,
-        # regions placed on GPUs by LPT on their point counts (strong scaling)
-        prob = make_config("C5", method=args.method)
+    elif args.workload in ("c3", "c4", "c5"):
+        # C3 Burgers x-t XPINN 4x2 (8 x 20k residual points), C4 NS cavity XPINN 4x2
+        # (8 x 125k, the 1M-point strong-scaling case), C5 inverse heat (10-region map):
+        # fixed decompositions, subdomains placed on GPUs by LPT on their point counts
+        # (strong scaling)
+        prob = make_config(args.workload.upper(), method=args.method,
+                           **({"gpus": 8} if args.workload == "c3" else {}))
         owner = lpt_owner([prob.n_points(q) for q in range(prob.n_sub)], world)
         local = [q for q in range(prob.n_sub) if owner[q] == rank]
         h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING)
@@ -347,8 +363,9 @@ def run_ours(args):
             traffic = None
 
     if rank == 0:
-        base_prob = make_config("C5", method=args.method) if args.workload == "c5" else \
-            make_config("C2", method=args.method)
+        base_prob = (make_config("C2", method=args.method) if args.workload == "c2" else
+                     make_config(args.workload.upper(), method=args.method,
+                                 **({"gpus": 8} if args.workload == "c3" else {})))
         base = (cpu_baseline(base_prob) if (world == 1 and not args.no_cpu and args.method != "dp") else None)
         acts = sorted({prob.act(q) for q in local})
         kname = (f"K1 k_fused<{prob.width},{prob.n_hidden},{prob.d_out},"
@@ -357,7 +374,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "iters_per_s": 1e3 * args.steps / t_max,
             "config": {"workload": f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}",
@@ -397,12 +414,13 @@ def main():
                     help="default cpinn for c2, xpinn for c5; dp = data-parallel vanilla PINN comparator "
                          "(Table 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--workload", choices=["c2", "c5"], default="c2",
-                    help="c2: BASELINE configs[1] (default, the headline); c5: inverse heat map (configs[4])")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c2",
+                    help="c2: BASELINE configs[1] (default, the headline); c3/c4/c5: configs[2..4] "
+                         "(fixed decompositions, strong scaling)")
     args = ap.parse_args()
     if args.method is None:
-        args.method = "xpinn" if args.workload == "c5" else "cpinn"
-    if args.workload == "c5" and args.method == "dp":
+        args.method = "cpinn" if args.workload == "c2" else "xpinn"
+    if args.workload != "c2" and args.method == "dp":
         raise SystemExit("--method dp is the C2 data-parallel comparator")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
