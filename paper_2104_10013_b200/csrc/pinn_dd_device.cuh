@@ -118,6 +118,26 @@ struct KCfg {
 // (Table 3) -- uniform per chunk, so the branch never diverges.
 // ----------------------------------------------------------------------------
 constexpr int kActMixed = 3;
+
+// sin and cos of x for |x| up to ~1e4: 3-term Cody-Waite reduction by pi/2 and
+// minimax polynomials on [-pi/4, pi/4] (~1e-7 relative).  Replaces sincosf,
+// whose Payne-Hanek slow path bloats the unrolled jet loops (instruction-cache
+// misses in the per-subdomain-activation kernel).
+__device__ __forceinline__ void fast_sincos(float x, float* sn, float* cs) {
+  const float k = rintf(x * 0.636619772f);
+  float r = fmaf(-k, 1.5703125f, x);
+  r = fmaf(-k, 4.837512969970703125e-4f, r);
+  r = fmaf(-k, 7.54978995489188216e-8f, r);
+  const float z = r * r;
+  const float s = fmaf(r * z, fmaf(z, fmaf(z, -1.9515295891e-4f, 8.3321608736e-3f), -1.6666654611e-1f), r);
+  const float co = fmaf(z * z, fmaf(z, fmaf(z, 2.443315711809948e-5f, -1.388731625493765e-3f), 4.166664568298827e-2f),
+                        fmaf(-0.5f, z, 1.0f));
+  const int q = int(k) & 3;
+  const float a = (q & 1) ? co : s;    // sin for q = 0, 2
+  const float b = (q & 1) ? s : co;    // cos for q = 0, 2
+  *sn = (q & 2) ? -a : a;
+  *cs = ((q + 1) & 2) ? -b : b;
+}
 template <int ACT>
 __device__ __forceinline__ int act_sel(int act) {
   return ACT == kActMixed ? act : ACT;
@@ -133,11 +153,11 @@ __device__ __forceinline__ void act_derivs(float u, float& s0, float& s1, float&
     s3 = s1 * (6.0f * t * t - 2.0f);
   } else if (A == 1) {
     float sn, cs;
-    sincosf(u, &sn, &cs);
+    fast_sincos(u, &sn, &cs);
     s0 = sn; s1 = cs; s2 = -sn; s3 = -cs;
   } else {
     float sn, cs;
-    sincosf(u, &sn, &cs);
+    fast_sincos(u, &sn, &cs);
     s0 = cs; s1 = -sn; s2 = -cs; s3 = sn;
   }
 }
@@ -419,6 +439,8 @@ struct KArgs {
   const int32_t* sub_act;   // [n_sub] activation per subdomain (read only by kActMixed instances)
   const float4* sub_w;      // [n_sub] (w_u, w_f, w_i, w_if)
   const Chunk* chunks;
+  const int32_t* order;     // [n_chunks] processing order (nullptr = identity)
+  int32_t* sched;           // [2] chunk counter, CTAs done (zero between launches)
   int n_chunks;
   int64_t n_points;
   int pstride;              // floats per subdomain in params / partial

@@ -123,7 +123,7 @@ struct pinn_dd {
   float *partial = nullptr, *partial_loss = nullptr, *payload = nullptr, *loss = nullptr;
   float *pinv = nullptr, *gstash = nullptr, *scratch = nullptr;
   int32_t *pinfo = nullptr, *ptwin = nullptr, *sub_chunk = nullptr, *tstep = nullptr, *done = nullptr;
-  int32_t *flag = nullptr, *packmap = nullptr, *sub_act = nullptr;
+  int32_t *flag = nullptr, *packmap = nullptr, *sub_act = nullptr, *order1 = nullptr, *sched = nullptr;
   float2* segn = nullptr;
   float4 *sub_w = nullptr, *sub_adam = nullptr;
   Chunk *chunks1 = nullptr, *chunks2 = nullptr;
@@ -169,6 +169,21 @@ int chunk_tiles(int cnt, int P) {
   return std::max(4, (tiles + 127) / 128);
 }
 
+// point counts of the K1 chunks of a subdomain with `cnt` points: full chunks
+// of chunk_tiles(cnt) tiles, the remainder as one-tile chunks (the schedule's
+// tail); depends only on cnt (placement invariance)
+void chunk_sizes(int cnt, int P, std::vector<int>& out) {
+  out.clear();
+  if (cnt == 0) {
+    out.push_back(0);
+    return;
+  }
+  const int span = chunk_tiles(cnt, P) * P;
+  int s0 = 0;
+  for (; s0 + span <= cnt; s0 += span) out.push_back(span);
+  for (; s0 < cnt; s0 += P) out.push_back(std::min(P, cnt - s0));
+}
+
 struct Carve {
   size_t off = 0;
   template <class T>
@@ -180,7 +195,8 @@ struct Carve {
 };
 
 struct Layout {
-  size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ch2, subch,
+  size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ord1,
+      sched, ch2, subch,
       tstep, done, flag, loss, packmap, gstash, total;
 };
 
@@ -265,10 +281,11 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   // fixed-order reduction is bitwise placement-invariant.
   const int P = ops->P;
   int n1 = 0, n2 = 0;
+  std::vector<int> sizes;
   for (int q = 0; q < d->n_sub; ++q) {
     const int cnt = d->sub_point_offset[q + 1] - d->sub_point_offset[q];
-    const int span = chunk_tiles(cnt, P) * P;
-    n1 += std::max(1, (cnt + span - 1) / span);
+    chunk_sizes(cnt, P, sizes);
+    n1 += int(sizes.size());
     const int ni = cnt - d->sub_n_res[q] - d->sub_n_data[q];
     n2 += (ni + P - 1) / P;
   }
@@ -294,6 +311,8 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->subact = c.take<int32_t>(ns);
   L->suba = c.take<float4>(ns);
   L->ch1 = c.take<Chunk>(size_t(n1));
+  L->ord1 = c.take<int32_t>(size_t(n1));
+  L->sched = c.take<int32_t>(4);
   L->ch2 = c.take<Chunk>(size_t(n2) + 1);
   L->subch = c.take<int32_t>(ns + 1);
   L->tstep = c.take<int32_t>(ns);
@@ -339,6 +358,8 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.sub_w = h->sub_w;
   a.sub_act = h->sub_act;
   a.chunks = payload_tiles ? h->chunks2 : h->chunks1;
+  a.order = payload_tiles ? nullptr : h->order1;
+  a.sched = h->sched + (payload_tiles ? 2 : 0);
   a.n_chunks = payload_tiles ? h->n_chunks2 : h->n_chunks1;
   a.n_points = d.n_points;
   a.pstride = h->pstride;
@@ -528,6 +549,8 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->sub_act = reinterpret_cast<int32_t*>(base + L.subact);
   h->sub_adam = reinterpret_cast<float4*>(base + L.suba);
   h->chunks1 = reinterpret_cast<Chunk*>(base + L.ch1);
+  h->order1 = reinterpret_cast<int32_t*>(base + L.ord1);
+  h->sched = reinterpret_cast<int32_t*>(base + L.sched);
   h->chunks2 = reinterpret_cast<Chunk*>(base + L.ch2);
   h->sub_chunk = reinterpret_cast<int32_t*>(base + L.subch);
   h->tstep = reinterpret_cast<int32_t*>(base + L.tstep);
@@ -594,14 +617,22 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   for (int q = 0; q < ns; ++q) {
     subch[q] = int32_t(c1.size());
     const int off = h->sub_off[q], cnt = h->sub_off[q + 1] - off;
-    const int span = chunk_tiles(cnt, P) * P;
-    if (cnt == 0) c1.push_back(Chunk{q, off, 0, 0});
-    for (int s0 = 0; s0 < cnt; s0 += span) c1.push_back(Chunk{q, off + s0, std::min(span, cnt - s0), 0});
+    std::vector<int> sizes;
+    chunk_sizes(cnt, P, sizes);
+    int s0 = 0;
+    for (int sz : sizes) {
+      c1.push_back(Chunk{q, off + s0, sz, 0});
+      s0 += sz;
+    }
     const int i0 = off + h->n_res[q] + h->n_data[q];
     const int ni = h->sub_off[q + 1] - i0;
     for (int s0 = 0; s0 < ni; s0 += P) c2.push_back(Chunk{q, i0 + s0, std::min(P, ni - s0), 0});
   }
   subch[ns] = int32_t(c1.size());
+  // K1 processing order: larger chunks first (stable), the one-tile tail last
+  std::vector<int32_t> ord1(c1.size());
+  for (size_t i = 0; i < ord1.size(); ++i) ord1[i] = int32_t(i);
+  std::stable_sort(ord1.begin(), ord1.end(), [&](int32_t x, int32_t y) { return c1[x].count > c1[y].count; });
   std::vector<int32_t> pm;
   h->ops->packmap(pm);
   h->n_packed = int(pm.size());
@@ -632,6 +663,8 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   CKC(cudaMemcpyAsync(h->sub_act, h->act.data(), h->act.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->sub_adam, suba.data(), suba.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->chunks1, c1.data(), c1.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->order1, ord1.data(), ord1.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemsetAsync(h->sched, 0, 4 * sizeof(int32_t), st));
   if (!c2.empty())
     CKC(cudaMemcpyAsync(h->chunks2, c2.data(), c2.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->sub_chunk, subch.data(), subch.size() * 4, cudaMemcpyHostToDevice, st));

@@ -319,13 +319,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
     }
   }
 
-  // contiguous chunk range per CTA: consecutive chunks mostly share a subdomain,
-  // so its weights are staged into shared memory once
-  const int c_beg = int((int64_t(a.n_chunks) * blockIdx.x) / gridDim.x);
-  const int c_end = int((int64_t(a.n_chunks) * (blockIdx.x + 1)) / gridDim.x);
+  // persistent CTAs take chunks from a global counter in `order` (largest
+  // chunks first, one-tile chunks last), so the tail is one tile long.  Which
+  // CTA runs a chunk never changes its result: every chunk owns its partial
+  // slot and K5 sums the slots in a fixed order.
+  __shared__ int s_next;
   int cur_sub = -1;
 #pragma unroll 1
-  for (int c = c_beg; c < c_end; ++c) {
+  for (;;) {
+    if (tid == 0) s_next = atomicAdd(a.sched, 1);
+    cta_sync();
+    const int idx = s_next;
+    if (idx >= a.n_chunks) break;
+    const int c = a.order ? a.order[idx] : idx;
     const Chunk ch = a.chunks[c];
     if (ch.sub != cur_sub) {
       cta_sync();
@@ -634,6 +640,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       // flush the chunk's gradient (slope slots stay 0; K5 fills them)
       cta_sync();
       for (int e = tid; e < C::ACC; e += kThreads) Pc[e] = sAcc[e];
+    }
+    cta_sync();   // every thread has read s_next before it is overwritten
+  }
+  // the last CTA to leave re-arms the counter for the next launch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(a.sched + 1, 1) == int(gridDim.x) - 1) {
+      a.sched[0] = 0;
+      a.sched[1] = 0;
+      __threadfence();
     }
   }
   if constexpr (MODE == 0) {
