@@ -171,6 +171,17 @@ pinn_dd_status pinn_dd_payload_buffer(pinn_dd* h, float** buf, int32_t* n_fields
    packed gradient. */
 pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev);
 
+/* The same computation in two stream-ordered halves, so that the payload
+   exchange with other ranks overlaps interior compute:
+   _interior runs K1 over the residual and training points (it reads no payload
+   row and may be enqueued before the exchange completes); _interface runs K1
+   over the interface points (needs the complete payload buffer) and K5(reduce)
+   with the outputs of pinn_dd_loss_grad.  K1's chunks never mix the two point
+   classes, so interior + interface gives pinn_dd_loss_grad's results bit for
+   bit. */
+pinn_dd_status pinn_dd_loss_grad_interior(pinn_dd* h);
+pinn_dd_status pinn_dd_loss_grad_interface(pinn_dd* h, float* loss_dev, float* grad_dev);
+
 /* K5(adam): one bias-corrected Adam step (beta1, beta2, eps, lr per subdomain)
    on every local subdomain with the gradient of the last pinn_dd_loss_grad. */
 pinn_dd_status pinn_dd_adam(pinn_dd* h);

@@ -29,7 +29,8 @@ FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING = 1, 2, 4
 
 EXPORTS = [
     "pinn_dd_n_params", "pinn_dd_workspace_size", "pinn_dd_create", "pinn_dd_interface_payload",
-    "pinn_dd_payload_buffer", "pinn_dd_loss_grad", "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict",
+    "pinn_dd_payload_buffer", "pinn_dd_loss_grad", "pinn_dd_loss_grad_interior", "pinn_dd_loss_grad_interface",
+    "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict",
     "pinn_dd_get_params", "pinn_dd_set_params", "pinn_dd_get_step", "pinn_dd_kernel_times",
     "pinn_dd_plan_info", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
 ]
@@ -85,6 +86,8 @@ def load_library(path: str = LIB_PATH):
     lib.pinn_dd_interface_payload.argtypes = [vp]
     lib.pinn_dd_payload_buffer.argtypes = [vp, C.POINTER(vp), C.POINTER(i32), C.POINTER(i64)]
     lib.pinn_dd_loss_grad.argtypes = [vp, vp, vp]
+    lib.pinn_dd_loss_grad_interior.argtypes = [vp]
+    lib.pinn_dd_loss_grad_interface.argtypes = [vp, vp, vp]
     lib.pinn_dd_adam.argtypes = [vp]
     lib.pinn_dd_step.argtypes = [vp, i32, f32p]
     lib.pinn_dd_predict.argtypes = [vp, vp, vp, i64, vp]
@@ -329,17 +332,35 @@ class PinnDD:
         self._check(self.lib.pinn_dd_step(self.h, int(n_iters), p))
         return out
 
+    def loss_grad_phased(self, exchange=None, want_grad: bool = True):
+        """pinn_dd_loss_grad in two halves: K1 over residual + training points,
+        then `exchange()` (if given; e.g. waits for the payload receives), then K1
+        over interface points + K5a.  Same results as loss_grad, bit for bit."""
+        loss = torch.empty(self.n_sub, 8, dtype=torch.float32, device=self.device)
+        grad = torch.empty(self.n_sub, self.n_params, dtype=torch.float32, device=self.device) if want_grad else None
+        self._check(self.lib.pinn_dd_loss_grad_interior(self.h))
+        if exchange is not None:
+            exchange()
+        self._check(self.lib.pinn_dd_loss_grad_interface(self.h, C.c_void_p(loss.data_ptr()),
+                                                         C.c_void_p(grad.data_ptr()) if want_grad else None))
+        return loss, grad
+
     def step_distributed(self, n_iters: int = 1, group=None, want_loss: bool = False):
         """Algorithm 1 with remote neighbours: payload (K2) ->
-        exchange with the neighbouring ranks -> loss + gradient (K1, K5a) -> Adam
-        (K5b).  Returns the last iteration's [n_sub, 8] loss breakdown (host) if
-        want_loss."""
+        non-blocking exchange with the neighbouring ranks, overlapped with K1 over
+        the residual and training points -> wait -> K1 over the interface points
+        and K5a -> Adam (K5b).  Returns the last iteration's [n_sub, 8] loss
+        breakdown (host) if want_loss."""
         if not hasattr(self, "_loss_dev"):
             self._loss_dev = torch.empty(self.n_sub, 8, dtype=torch.float32, device=self.device)
         for _ in range(n_iters):
             self.interface_payload()
-            exchange_payload(self.payload, self.table.plan, group)
-            self._check(self.lib.pinn_dd_loss_grad(self.h, C.c_void_p(self._loss_dev.data_ptr()), None))
+            reqs = exchange_payload(self.payload, self.table.plan, group, wait=False)
+            self._check(self.lib.pinn_dd_loss_grad_interior(self.h))
+            for r in reqs:
+                r.wait()
+            self._check(self.lib.pinn_dd_loss_grad_interface(self.h, C.c_void_p(self._loss_dev.data_ptr()),
+                                                             None))
             self.adam()
         return self._loss_dev.cpu().numpy() if want_loss else None
 
@@ -384,13 +405,16 @@ class PinnDD:
         return list(v)
 
 
-def exchange_payload(payload: torch.Tensor, plan: ExchangePlan, group=None):
+def exchange_payload(payload: torch.Tensor, plan: ExchangePlan, group=None, wait: bool = True):
     """Green stage of Algorithm 1: non-blocking send/recv of the cut-edge payload
-    rows with every neighbouring rank, then wait.
-    Works on CUDA tensors with NCCL and on CPU tensors with gloo."""
+    rows with every neighbouring rank; waits unless
+    wait=False, in which case the request handles are returned (NCCL: waiting
+    makes the current stream wait, so interior compute enqueued before it
+    overlaps the transfer).  Works on CUDA tensors with NCCL and on CPU tensors
+    with gloo."""
     import torch.distributed as dist
     if not plan.send and not plan.recv:
-        return
+        return []
     ops, bufs = [], []
     cache = plan.__dict__.setdefault("_idx_cache", {})
     for peer in sorted(set(plan.send) | set(plan.recv)):
@@ -405,8 +429,12 @@ def exchange_payload(payload: torch.Tensor, plan: ExchangePlan, group=None):
         if peer in plan.recv:
             r0, n = plan.recv[peer]
             ops.append(dist.P2POp(dist.irecv, payload[r0:r0 + n], peer, group))
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
+    reqs = dist.batch_isend_irecv(ops)
+    if wait:
+        for req in reqs:
+            req.wait()
+        return []
+    return reqs
 
 
 # ---------------------------------------------------------------------------

@@ -117,7 +117,7 @@ struct pinn_dd {
   int nf = 0, neq = 0, n_packed = 0, pstride = 0;
   int nsm = 148;
   // plan
-  int n_chunks1 = 0, n_chunks2 = 0, grid1 = 0, grid2 = 0, tpc = 1;
+  int n_chunks1 = 0, n_chunks2 = 0, grid1 = 0, grid2 = 0, tpc = 1, n_int = 0;
   // device (carved from the workspace)
   float *params = nullptr, *m = nullptr, *v = nullptr, *grad = nullptr;
   float *partial = nullptr, *partial_loss = nullptr, *payload = nullptr, *loss = nullptr;
@@ -169,19 +169,29 @@ int chunk_tiles(int cnt, int P) {
   return std::max(4, (tiles + 127) / 128);
 }
 
-// point counts of the K1 chunks of a subdomain with `cnt` points: full chunks
-// of chunk_tiles(cnt) tiles, the remainder as one-tile chunks (the schedule's
+// point counts of the K1 chunks of a run of `cnt` points: full chunks of
+// chunk_tiles(cnt) tiles, the remainder as one-tile chunks (the schedule's
 // tail); depends only on cnt (placement invariance)
 void chunk_sizes(int cnt, int P, std::vector<int>& out) {
-  out.clear();
-  if (cnt == 0) {
-    out.push_back(0);
-    return;
-  }
+  if (cnt == 0) return;
   const int span = chunk_tiles(cnt, P) * P;
   int s0 = 0;
   for (; s0 + span <= cnt; s0 += span) out.push_back(span);
   for (; s0 < cnt; s0 += P) out.push_back(std::min(P, cnt - s0));
+}
+
+// K1 chunks of a subdomain: its `na` residual + training points, then its `ni`
+// interface points (a chunk never mixes the two, so the interface part can run
+// after the payload exchange); sign of the entry = interface run.
+// An empty subdomain still gets one (empty) chunk and thus a partial slot.
+std::vector<int> split_chunks(int na, int ni, int P) {
+  std::vector<int> a, b;
+  chunk_sizes(na, P, a);
+  chunk_sizes(ni, P, b);
+  for (int& v : b) v = -v - 1;
+  a.insert(a.end(), b.begin(), b.end());
+  if (a.empty()) a.push_back(0);
+  return a;
 }
 
 struct Carve {
@@ -284,8 +294,8 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   std::vector<int> sizes;
   for (int q = 0; q < d->n_sub; ++q) {
     const int cnt = d->sub_point_offset[q + 1] - d->sub_point_offset[q];
-    chunk_sizes(cnt, P, sizes);
-    n1 += int(sizes.size());
+    const int na = d->sub_n_res[q] + d->sub_n_data[q];
+    n1 += int(split_chunks(na, cnt - na, P).size());
     const int ni = cnt - d->sub_n_res[q] - d->sub_n_data[q];
     n2 += (ni + P - 1) / P;
   }
@@ -311,7 +321,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->subact = c.take<int32_t>(ns);
   L->suba = c.take<float4>(ns);
   L->ch1 = c.take<Chunk>(size_t(n1));
-  L->ord1 = c.take<int32_t>(size_t(n1));
+  L->ord1 = c.take<int32_t>(size_t(2 * n1));   // [all | interior, interface] processing orders
   L->sched = c.take<int32_t>(4);
   L->ch2 = c.take<Chunk>(size_t(n2) + 1);
   L->subch = c.take<int32_t>(ns + 1);
@@ -358,7 +368,7 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.sub_w = h->sub_w;
   a.sub_act = h->sub_act;
   a.chunks = payload_tiles ? h->chunks2 : h->chunks1;
-  a.order = payload_tiles ? nullptr : h->order1;
+  a.order = payload_tiles ? nullptr : h->order1;   // launch_k1 selects the part
   a.sched = h->sched + (payload_tiles ? 2 : 0);
   a.n_chunks = payload_tiles ? h->n_chunks2 : h->n_chunks1;
   a.n_points = d.n_points;
@@ -406,8 +416,19 @@ pinn_dd_status launch_k2(pinn_dd* h) {
   CK(h, cudaGetLastError());
   return PINN_DD_OK;
 }
-pinn_dd_status launch_k1(pinn_dd* h) {
-  h->ops->k1(make_kargs(h, false), h->grid1, h->ops->smem, h->stream);
+// part 0: every K1 chunk; 1: residual + training chunks; 2: interface chunks
+pinn_dd_status launch_k1(pinn_dd* h, int part = 0) {
+  KArgs a = make_kargs(h, false);
+  const int n1 = h->n_chunks1;
+  if (part == 1) {
+    a.order = h->order1 + n1;
+    a.n_chunks = h->n_int;
+  } else if (part == 2) {
+    a.order = h->order1 + n1 + h->n_int;
+    a.n_chunks = n1 - h->n_int;
+  }
+  if (a.n_chunks == 0) return PINN_DD_OK;
+  h->ops->k1(a, std::min(h->grid1, a.n_chunks), h->ops->smem, h->stream);
   ++h->launches;
   CK(h, cudaGetLastError());
   return PINN_DD_OK;
@@ -617,11 +638,12 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   for (int q = 0; q < ns; ++q) {
     subch[q] = int32_t(c1.size());
     const int off = h->sub_off[q], cnt = h->sub_off[q + 1] - off;
-    std::vector<int> sizes;
-    chunk_sizes(cnt, P, sizes);
+    const int na = h->n_res[q] + h->n_data[q];
     int s0 = 0;
-    for (int sz : sizes) {
-      c1.push_back(Chunk{q, off + s0, sz, 0});
+    for (int sz : split_chunks(na, cnt - na, P)) {
+      const bool iface = sz < 0;
+      if (iface) sz = -sz - 1;
+      c1.push_back(Chunk{q, off + s0, sz, iface ? 1 : 0});
       s0 += sz;
     }
     const int i0 = off + h->n_res[q] + h->n_data[q];
@@ -629,10 +651,22 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
     for (int s0 = 0; s0 < ni; s0 += P) c2.push_back(Chunk{q, i0 + s0, std::min(P, ni - s0), 0});
   }
   subch[ns] = int32_t(c1.size());
-  // K1 processing order: larger chunks first (stable), the one-tile tail last
-  std::vector<int32_t> ord1(c1.size());
-  for (size_t i = 0; i < ord1.size(); ++i) ord1[i] = int32_t(i);
-  std::stable_sort(ord1.begin(), ord1.end(), [&](int32_t x, int32_t y) { return c1[x].count > c1[y].count; });
+  // K1 processing orders, larger chunks first (stable), the one-tile tail last:
+  // [0, n1) every chunk (pinn_dd_loss_grad); [n1, n1 + n_int) residual/training
+  // chunks, then [n1 + n_int, 2 n1) interface chunks (the phased calls)
+  std::vector<int32_t> ord1(2 * c1.size());
+  auto big_first = [&](int32_t x, int32_t y) { return c1[x].count > c1[y].count; };
+  for (size_t i = 0; i < c1.size(); ++i) ord1[i] = int32_t(i);
+  std::stable_sort(ord1.begin(), ord1.begin() + c1.size(), big_first);
+  int n_int = 0;
+  for (size_t i = 0; i < c1.size(); ++i)
+    if (!c1[i].pad) ord1[c1.size() + n_int++] = int32_t(i);
+  int k = n_int;
+  for (size_t i = 0; i < c1.size(); ++i)
+    if (c1[i].pad) ord1[c1.size() + k++] = int32_t(i);
+  std::stable_sort(ord1.begin() + c1.size(), ord1.begin() + c1.size() + n_int, big_first);
+  std::stable_sort(ord1.begin() + c1.size() + n_int, ord1.end(), big_first);
+  h->n_int = n_int;
   std::vector<int32_t> pm;
   h->ops->packmap(pm);
   h->n_packed = int(pm.size());
@@ -717,11 +751,9 @@ pinn_dd_status pinn_dd_payload_buffer(pinn_dd* h, float** buf, int32_t* n_fields
   return PINN_DD_OK;
 }
 
-pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev) {
-  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+// K5a (reduce + slopes) and the optional copies of pinn_dd_loss_grad
+static pinn_dd_status finish_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev) {
   pinn_dd_status s;
-  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h)) != PINN_DD_OK || (s = phase_end(h, 1)) != PINN_DD_OK)
-    return s;
   if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k5(h, 0)) != PINN_DD_OK || (s = phase_end(h, 2)) != PINN_DD_OK)
     return s;
   if (loss_dev)
@@ -733,6 +765,29 @@ pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev) {
     CK(h, cudaGetLastError());
   }
   return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  pinn_dd_status s;
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h)) != PINN_DD_OK || (s = phase_end(h, 1)) != PINN_DD_OK)
+    return s;
+  return finish_loss_grad(h, loss_dev, grad_dev);
+}
+
+pinn_dd_status pinn_dd_loss_grad_interior(pinn_dd* h) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  pinn_dd_status s;
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h, 1)) != PINN_DD_OK) return s;
+  return phase_end(h, 1);
+}
+
+pinn_dd_status pinn_dd_loss_grad_interface(pinn_dd* h, float* loss_dev, float* grad_dev) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  pinn_dd_status s;
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h, 2)) != PINN_DD_OK || (s = phase_end(h, 1)) != PINN_DD_OK)
+    return s;
+  return finish_loss_grad(h, loss_dev, grad_dev);
 }
 
 pinn_dd_status pinn_dd_adam(pinn_dd* h) {

@@ -269,6 +269,42 @@ def test_placement_invariance_two_handles():
         h.close()
 
 
+def test_phased_loss_grad_overlapping_the_exchange():
+    """K1 over residual + training points is enqueued BEFORE the
+    remote payload rows arrive (they are poisoned with NaN until then); the
+    interface half after the 'exchange'.  Bitwise equal to the one-handle
+    pinn_dd_loss_grad (and to the same handle's own fused call)."""
+    from paper_2104_10013_b200.binding import PinnDD
+    prob = perturb_params(make_config("C2", method="cpinn", n_f=300, n_i=25, n_u=20), scale=0.1)
+    one = PinnDD(prob, device="cuda:0")
+    one.interface_payload()
+    l1, g1 = one.loss_grad()
+    l1b, g1b = one.loss_grad_phased()
+    torch.cuda.synchronize()
+    assert torch.equal(l1, l1b) and torch.equal(g1, g1b)
+    owner = [0 if s.ix < 2 else 1 for s in prob.subdomains]
+    hs = [PinnDD(prob, [q for q in range(16) if owner[q] == r], owner, r, device="cuda:0") for r in (0, 1)]
+    for h in hs:
+        h.interface_payload()
+    outs = []
+    for r, h in enumerate(hs):
+        o = hs[1 - r]
+        r0, n = h.table.plan.recv[1 - r]
+        idx = torch.as_tensor(o.table.plan.send[r], device="cuda:0")
+        h.payload[r0:r0 + n] = float("nan")
+
+        def exchange(h=h, o=o, r0=r0, n=n, idx=idx):
+            h.payload[r0:r0 + n] = o.payload.index_select(0, idx)
+        outs.append(h.loss_grad_phased(exchange))
+    torch.cuda.synchronize()
+    for r, h in enumerate(hs):
+        for i, q in enumerate(h.table.local):
+            assert torch.equal(outs[r][0][i], l1[q]), (r, q)
+            assert torch.equal(outs[r][1][i], g1[q]), (r, q)
+    for h in hs + [one]:
+        h.close()
+
+
 def test_predict_stitching():
     prob = make_config("C3", method="xpinn", gpus=4, n_f=100, n_i=10, n_u=10)
     m = _handle(prob)
