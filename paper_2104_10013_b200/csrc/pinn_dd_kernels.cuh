@@ -347,6 +347,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       for (int e = tid; e < C::ACC; e += kThreads) sAcc[e] = 0.0f;
     }
     const int ntiles = (ch.count + C::P - 1) / C::P;
+    if constexpr (MODE == 0) {
+      if (ntiles == 0) {   // a subdomain without points: its slot holds zeros
+        if (!DSM)
+          for (int e = tid; e < a.pstride; e += kThreads) Pc[e] = 0.0f;
+        if (tid < 4) a.partial_loss[size_t(c) * 4 + tid] = 0.0f;
+      }
+    }
 #pragma unroll 1
     for (int t = 0; t < ntiles; ++t) {
       const int64_t p0 = int64_t(ch.start) + int64_t(t) * C::P;

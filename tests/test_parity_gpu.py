@@ -430,6 +430,23 @@ def test_train_cpinn_poisson_to_accuracy():
     m.close()
 
 
+def test_degenerate_point_sets():
+    """Edge cases: subdomains with interface points only (N_F = N_u = 0, so
+    MSE_F = MSE_u = 0, Z14), a ragged single-tile case, and a subdomain with
+    no points at all (J = 0, zero gradient, Adam leaves it unchanged)."""
+    run_parity(make_config("C2", method="xpinn", n_f=0, n_i=7, n_u=0), "interface only")
+    run_parity(make_config("C1", n_f=1, n_i=1, n_u=1), "one point per class")
+    prob = make_config("C2", method="pinn", nx=1, ny=1, n_f=0, n_u=0)
+    m = _handle(prob)
+    loss, grad = m.loss_grad()
+    th0 = m.get(0).clone()
+    m.adam()
+    torch.cuda.synchronize()
+    assert torch.all(loss == 0) and torch.all(grad == 0)
+    assert torch.equal(m.get(0), th0)
+    m.close()
+
+
 def test_nonfinite_is_reported():
     from paper_2104_10013_b200.binding import PinnDDError, ENONFINITE
     prob = make_config("C1", n_f=100, n_i=10, n_u=20)
