@@ -80,6 +80,8 @@ enum { PINN_DD_ACT_TANH = 0, PINN_DD_ACT_SIN = 1, PINN_DD_ACT_COS = 2 };
 #define PINN_DD_FLAG_GRAPH        1  /* pinn_dd_step replays a captured CUDA graph */
 #define PINN_DD_FLAG_GLOBAL_STASH 2  /* keep the reverse-mode stash in global memory instead of TMEM (debug) */
 #define PINN_DD_FLAG_TIMING       4  /* record per-kernel CUDA events (see pinn_dd_kernel_times) */
+#define PINN_DD_FLAG_POINT_PER_THREAD 8 /* width-20 nets: one thread per point (all neurons in
+                                           registers) instead of the default neuron-block kernel */
 
 /* Per-subdomain hyper-parameters, P:151-161 (loss weights) and P:286 (Adam). */
 typedef struct {

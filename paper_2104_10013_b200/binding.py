@@ -25,7 +25,7 @@ OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, ENONFINITE, EPROTOCOL = range(7)
 METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2, "hybrid": 3}
 PDES = {"burgers": 0, "poisson": 1, "heat": 2, "ns": 3, "heat_inv": 4}
 ACTS = {"tanh": 0, "sin": 1, "cos": 2}
-FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING = 1, 2, 4
+FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING, FLAG_POINT_PER_THREAD = 1, 2, 4, 8
 
 EXPORTS = [
     "pinn_dd_n_params", "pinn_dd_workspace_size", "pinn_dd_create", "pinn_dd_interface_payload",

@@ -18,6 +18,7 @@
 
 #include "../../include/pinn_dd.h"
 #include "pinn_dd_kernels.cuh"
+#include "pinn_dd_kernels_pt.cuh"
 
 using namespace pinn;
 
@@ -30,6 +31,7 @@ thread_local std::string g_create_error;
 // -------------------------------------------------------------------------
 struct Ops {
   int N, NH, DO, ACT;
+  int pt;          // 1: point-per-thread kernel (narrow nets), 0: neuron-block kernel
   int pstride;     // Lay::total()
   int P;           // points per tile
   size_t smem;     // dynamic smem of the fused kernel
@@ -42,16 +44,27 @@ struct Ops {
   cudaError_t (*setattr)(size_t);
 };
 
-template <int N, int NH, int DO, int ACT>
+template <int N, int NH, int DO, int ACT, bool PT = false>
 struct Inst {
   using C = KCfg<N, NH, DO>;
   using LY = Lay<N, NH, DO>;
-  static size_t smem() { return std::max<size_t>(C::SMEM, 120 * 1024); }   // force 1 CTA / SM (TMEM owner)
+  static size_t smem() {   // >= 120 KB forces 1 CTA / SM (the CTA owns all of TMEM)
+    if constexpr (PT)
+      return std::max<size_t>(PtCfg<N, NH, DO>::SMEM, 120 * 1024);
+    else
+      return std::max<size_t>(C::SMEM, 120 * 1024);
+  }
   static void k1(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
-    k_fused<N, NH, DO, ACT, 0><<<grid, kThreads, sm, s>>>(a);
+    if constexpr (PT)
+      k_fused_pt<N, NH, DO, ACT, 0><<<grid, kPT, sm, s>>>(a);
+    else
+      k_fused<N, NH, DO, ACT, 0><<<grid, kThreads, sm, s>>>(a);
   }
   static void k2(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
-    k_fused<N, NH, DO, ACT, 1><<<grid, kThreads, sm, s>>>(a);
+    if constexpr (PT)
+      k_fused_pt<N, NH, DO, ACT, 1><<<grid, kPT, sm, s>>>(a);
+    else
+      k_fused<N, NH, DO, ACT, 1><<<grid, kThreads, sm, s>>>(a);
   }
   static void pred(const float* params, int pstride, float sn, const float* pts, const int32_t* own, int64_t n,
                    float* out, const int32_t* sub_act, cudaStream_t s) {
@@ -81,26 +94,40 @@ struct Inst {
     }
   }
   static cudaError_t setattr(size_t sm) {
-    cudaError_t e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(sm));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e;
+    if constexpr (PT) {
+      e = cudaFuncSetAttribute(k_fused_pt<N, NH, DO, ACT, 0>, attr, int(sm));
+      if (e != cudaSuccess) return e;
+      return cudaFuncSetAttribute(k_fused_pt<N, NH, DO, ACT, 1>, attr, int(sm));
+    } else {
+      e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0>, attr, int(sm));
+      if (e != cudaSuccess) return e;
+      return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1>, attr, int(sm));
+    }
   }
   static Ops ops() {
     static_assert(NH <= kMaxHidden, "too many hidden layers");
-    return Ops{N, NH, DO, ACT, LY::total(), C::P, smem(), &k1, &k2, &pred, &packmap, &slopetab, &setattr};
+    if constexpr (PT) static_assert(PtCfg<N, NH, DO>::P == C::P, "both kernels tile by the same point count");
+    return Ops{N, NH, DO, ACT, PT ? 1 : 0, LY::total(), C::P, smem(), &k1, &k2, &pred, &packmap, &slopetab,
+               &setattr};
   }
 };
 
 // The shapes of BASELINE.json configs C1-C4 (tanh): 3x20, 5x20, 6x40, 5x80 (D_o = 3);
 // C5 (inverse heat, outputs (T, K)): 3x80 with tanh / sin / cos per region (Table 3).
-const Ops* find_ops(int N, int NH, int DO, int ACT) {
+// Width-20 nets also have the point-per-thread kernel (pt = 1), selected with
+// PINN_DD_FLAG_POINT_PER_THREAD; the neuron-block kernel is the default (faster
+// on the B200).
+const Ops* find_ops(int N, int NH, int DO, int ACT, int pt = -1) {
   static const Ops table[] = {
-      Inst<20, 3, 1, 0>::ops(), Inst<20, 5, 1, 0>::ops(), Inst<40, 6, 1, 0>::ops(), Inst<80, 5, 3, 0>::ops(),
+      Inst<20, 3, 1, 0, true>::ops(), Inst<20, 5, 1, 0, true>::ops(),
+      Inst<20, 3, 1, 0>::ops(),       Inst<20, 5, 1, 0>::ops(),
+      Inst<40, 6, 1, 0>::ops(),       Inst<80, 5, 3, 0>::ops(),
       Inst<80, 3, 2, kActMixed>::ops(),
   };
   for (const Ops& o : table)
-    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT) return &o;
+    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT && (pt < 0 || o.pt == pt)) return &o;
   return nullptr;
 }
 
@@ -230,8 +257,12 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   }
   const int act0 = d->sub_activation ? d->sub_activation[0] : d->activation;
   // one compiled activation if uniform, else the per-subdomain (kActMixed) instance
-  const Ops* ops = mixed ? nullptr : find_ops(d->width, d->n_hidden, d->d_out, act0);
-  if (!ops) ops = find_ops(d->width, d->n_hidden, d->d_out, kActMixed);
+  const int want_pt = (d->flags & PINN_DD_FLAG_POINT_PER_THREAD) ? 1 : 0;
+  const Ops* ops = nullptr;
+  for (int pt = want_pt; pt >= 0 && !ops; --pt) {   // no point-per-thread instance: neuron blocks
+    ops = mixed ? nullptr : find_ops(d->width, d->n_hidden, d->d_out, act0, pt);
+    if (!ops) ops = find_ops(d->width, d->n_hidden, d->d_out, kActMixed, pt);
+  }
   if (!ops)
     return fail(h, PINN_DD_EUNSUPPORTED, "network [2, %dx%d, %d] activation %d%s not compiled in", d->width,
                 d->n_hidden, d->d_out, act0, mixed ? " (mixed per subdomain)" : "");

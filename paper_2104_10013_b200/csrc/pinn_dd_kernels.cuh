@@ -271,6 +271,92 @@ __device__ __forceinline__ void st4(float* v, int jj, float4 x) {
   v[jj] = x.x; v[kJT + jj] = x.y; v[2 * kJT + jj] = x.z; v[3 * kJT + jj] = x.w;
 }
 
+// epilogue of one point (K2): u(x_I) and f.n (cPINN) or F (XPINN) into its
+// payload row (Algorithm 1)
+template <int DO>
+__device__ __forceinline__ void point_payload(const KArgs& a, int64_t gp, float x, float y, const float4* U) {
+  constexpr int NF = DO + (DO == 3 ? 3 : 1);
+  float r[3];
+  float dr[3][DO][4];
+  int ne;
+  const int info = a.pinfo[gp];
+  if (info & 4) {
+    const float2 n = a.seg_normal[info >> 3];
+    ne = pde_flux<DO>(a.pc, U, x, y, n.x, n.y, r, dr);
+  } else {
+    ne = pde_residual<DO>(a.pc, U, x, y, r, dr);
+  }
+  float* q = a.payload + size_t(gp) * NF;
+#pragma unroll
+  for (int o = 0; o < DO; ++o) q[o] = U[o].x;
+  for (int e = 0; e < ne; ++e) q[DO + e] = r[e];
+}
+
+// epilogue of one point (K1): its loss terms (Eq. 3/5/6; lsum = MSE_u, MSE_F,
+// MSE_uavg, MSE_if partials) and the adjoint seeds Ub = dJ/dU (a8)
+template <int DO>
+__device__ __forceinline__ void point_adjoint(const KArgs& a, int64_t gp, float x, float y, float4 lw,
+                                              const float4* U, float4* Ub, float* lsum) {
+  constexpr int NF = DO + (DO == 3 ? 3 : 1);
+  const int info = a.pinfo[gp];
+  const int kind = info & 3;
+  const float inv = a.pinv[gp];
+  float r[3];
+  float dr[3][DO][4];
+  if (kind == 0) {
+    // residual point: W_F (1/N_F) sum_e F_e^2
+    const int ne = pde_residual<DO>(a.pc, U, x, y, r, dr);
+    for (int e = 0; e < ne; ++e) {
+      lsum[1] += inv * r[e] * r[e];
+      const float cf = 2.0f * lw.y * inv * r[e];
+#pragma unroll
+      for (int o = 0; o < DO; ++o) {
+        Ub[o].x = fmaf(cf, dr[e][o][0], Ub[o].x);
+        Ub[o].y = fmaf(cf, dr[e][o][1], Ub[o].y);
+        Ub[o].z = fmaf(cf, dr[e][o][2], Ub[o].z);
+        Ub[o].w = fmaf(cf, dr[e][o][3], Ub[o].w);
+      }
+    }
+  } else if (kind == 1) {
+    // training point: W_u (1/N_u) sum_o mask_o |u^(i)_o - u_o|^2
+#pragma unroll
+    for (int o = 0; o < DO; ++o) {
+      const float m = a.mask[size_t(o) * a.n_points + gp];
+      const float d = m * (U[o].x - a.target[size_t(o) * a.n_points + gp]);
+      lsum[0] += inv * d * d;
+      Ub[o].x += 2.0f * lw.x * inv * d;
+    }
+  } else {
+    // interface point: neighbour payload is a constant
+    const float* q = a.payload + size_t(a.ptwin[gp]) * NF;
+#pragma unroll
+    for (int o = 0; o < DO; ++o) {
+      const float d = U[o].x - q[o];   // u_q - {{u}} = d / 2  (Z1)
+      lsum[2] += inv * 0.25f * d * d;
+      Ub[o].x += 0.5f * lw.z * inv * d;
+    }
+    int ne;
+    if (info & 4) {
+      const float2 n = a.seg_normal[info >> 3];
+      ne = pde_flux<DO>(a.pc, U, x, y, n.x, n.y, r, dr);
+    } else {
+      ne = pde_residual<DO>(a.pc, U, x, y, r, dr);
+    }
+    for (int e = 0; e < ne; ++e) {
+      const float d = r[e] - q[DO + e];
+      lsum[3] += inv * d * d;
+      const float cf = 2.0f * lw.w * inv * d;
+#pragma unroll
+      for (int o = 0; o < DO; ++o) {
+        Ub[o].x = fmaf(cf, dr[e][o][0], Ub[o].x);
+        Ub[o].y = fmaf(cf, dr[e][o][1], Ub[o].y);
+        Ub[o].z = fmaf(cf, dr[e][o][2], Ub[o].z);
+        Ub[o].w = fmaf(cf, dr[e][o][3], Ub[o].w);
+      }
+    }
+  }
+}
+
 template <int N, int NH, int DO, int ACT, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
   using C = KCfg<N, NH, DO>;
@@ -297,7 +383,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
   constexpr bool DSM = C::DW_SMEM;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::TOTAL - 4);
   const float m1 = a.m1, m2 = a.m2;
-  constexpr int NF = DO + (DO == 3 ? 3 : 1);
 
   Stash st;
   st.tid = tid;
@@ -427,24 +512,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       if constexpr (MODE == 1) {
         // payload: u(x_I) and f.n (cPINN) or F (XPINN) (Algorithm 1)
         for (int p = tid; p < np; p += kThreads) {
-          const int64_t gp = p0 + p;
           float4 U[DO];
 #pragma unroll
           for (int o = 0; o < DO; ++o) U[o] = sU[p * DO + o];
-          float r[3];
-          float dr[3][DO][4];
-          int ne;
-          const int info = a.pinfo[gp];
-          if (info & 4) {
-            const float2 n = a.seg_normal[info >> 3];
-            ne = pde_flux<DO>(a.pc, U, sX[p], sY[p], n.x, n.y, r, dr);
-          } else {
-            ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);
-          }
-          float* q = a.payload + size_t(gp) * NF;
-#pragma unroll
-          for (int o = 0; o < DO; ++o) q[o] = U[o].x;
-          for (int e = 0; e < ne; ++e) q[DO + e] = r[e];
+          point_payload<DO>(a, p0 + p, sX[p], sY[p], U);
         }
         continue;
       } else {
@@ -456,66 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
             U[o] = sU[p * DO + o];
             Ub[o] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
           }
-          if (p < np) {
-            const int64_t gp = p0 + p;
-            const int info = a.pinfo[gp];
-            const int kind = info & 3;
-            const float inv = a.pinv[gp];
-            float r[3];
-            float dr[3][DO][4];
-            if (kind == 0) {
-              // residual point: W_F (1/N_F) sum_e F_e^2
-              const int ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);
-              for (int e = 0; e < ne; ++e) {
-                lsum[1] += inv * r[e] * r[e];
-                const float cf = 2.0f * lw.y * inv * r[e];
-#pragma unroll
-                for (int o = 0; o < DO; ++o) {
-                  Ub[o].x = fmaf(cf, dr[e][o][0], Ub[o].x);
-                  Ub[o].y = fmaf(cf, dr[e][o][1], Ub[o].y);
-                  Ub[o].z = fmaf(cf, dr[e][o][2], Ub[o].z);
-                  Ub[o].w = fmaf(cf, dr[e][o][3], Ub[o].w);
-                }
-              }
-            } else if (kind == 1) {
-              // training point: W_u (1/N_u) sum_o mask_o |u^(i)_o - u_o|^2
-#pragma unroll
-              for (int o = 0; o < DO; ++o) {
-                const float m = a.mask[size_t(o) * a.n_points + gp];
-                const float d = m * (U[o].x - a.target[size_t(o) * a.n_points + gp]);
-                lsum[0] += inv * d * d;
-                Ub[o].x += 2.0f * lw.x * inv * d;
-              }
-            } else {
-              // interface point: neighbour payload is a constant
-              const float* q = a.payload + size_t(a.ptwin[gp]) * NF;
-#pragma unroll
-              for (int o = 0; o < DO; ++o) {
-                const float d = U[o].x - q[o];   // u_q - {{u}} = d / 2  (Z1)
-                lsum[2] += inv * 0.25f * d * d;
-                Ub[o].x += 0.5f * lw.z * inv * d;
-              }
-              int ne;
-              if (info & 4) {
-                const float2 n = a.seg_normal[info >> 3];
-                ne = pde_flux<DO>(a.pc, U, sX[p], sY[p], n.x, n.y, r, dr);
-              } else {
-                ne = pde_residual<DO>(a.pc, U, sX[p], sY[p], r, dr);
-              }
-              for (int e = 0; e < ne; ++e) {
-                const float d = r[e] - q[DO + e];
-                lsum[3] += inv * d * d;
-                const float cf = 2.0f * lw.w * inv * d;
-#pragma unroll
-                for (int o = 0; o < DO; ++o) {
-                  Ub[o].x = fmaf(cf, dr[e][o][0], Ub[o].x);
-                  Ub[o].y = fmaf(cf, dr[e][o][1], Ub[o].y);
-                  Ub[o].z = fmaf(cf, dr[e][o][2], Ub[o].z);
-                  Ub[o].w = fmaf(cf, dr[e][o][3], Ub[o].w);
-                }
-              }
-            }
-          }
+          if (p < np) point_adjoint<DO>(a, p0 + p, sX[p], sY[p], lw, U, Ub, lsum);
 #pragma unroll
           for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
         }

@@ -129,6 +129,41 @@ def test_loss_grad_parity_perturbed(cfg, kw):
     run_parity(prob, f"perturbed {cfg}")
 
 
+@pytest.mark.parametrize("cfg,kw", [CASES[0], CASES[1], CASES[5], CASES[9]])
+def test_width20_point_per_thread_kernel_parity(cfg, kw):
+    """Width-20 nets also compile the point-per-thread kernel
+    (PINN_DD_FLAG_POINT_PER_THREAD): it must match the oracle, and the two
+    kernels must agree to FP32 rounding."""
+    from paper_2104_10013_b200.binding import FLAG_GRAPH, FLAG_POINT_PER_THREAD
+    prob = perturb_params(make_config(cfg, **kw), scale=0.1)
+    run_parity(prob, f"point-per-thread {cfg}", flags=FLAG_GRAPH | FLAG_POINT_PER_THREAD)
+    outs = []
+    for fl in (FLAG_GRAPH, FLAG_GRAPH | FLAG_POINT_PER_THREAD):
+        m = _handle(prob, flags=fl)
+        m.interface_payload()
+        outs.append(m.loss_grad())
+        torch.cuda.synchronize()
+        m.close()
+    (la, ga), (lb, gb) = outs
+    assert torch.allclose(la, lb, rtol=1e-5, atol=1e-7)
+    assert torch.allclose(ga, gb, rtol=1e-4, atol=1e-5 * float(ga.abs().max()))
+
+
+def test_global_stash_point_per_thread_bitwise():
+    """The point-per-thread kernel's TMEM stash and its global-memory fallback
+    give bitwise identical results."""
+    from paper_2104_10013_b200.binding import FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_POINT_PER_THREAD
+    prob = perturb_params(make_config("C3", method="xpinn", gpus=4, n_f=300, n_i=20, n_u=30), scale=0.1)
+    outs = []
+    for fl in (FLAG_GRAPH | FLAG_POINT_PER_THREAD, FLAG_GRAPH | FLAG_GLOBAL_STASH | FLAG_POINT_PER_THREAD):
+        m = _handle(prob, flags=fl)
+        m.interface_payload()
+        outs.append(m.loss_grad())
+        torch.cuda.synchronize()
+        m.close()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
 def test_pinn_method_single_subdomain():
     prob = make_config("C2", method="pinn", nx=1, ny=1, n_f=500, n_u=64)
     run_parity(prob, "pinn")
