@@ -254,13 +254,16 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
+    # per-kernel CUDA events (FLAG_TIMING) only at N = 1, where they are graph
+    # nodes; the phased multi-GPU calls would synchronise the host per phase
+    tflag = FLAG_TIMING if world == 1 else 0
     if args.method == "dp":
         # data-parallel vanilla PINN comparator: one 6x40 network on
         # [0,G]x[0,1] with C2's point count per GPU, points sharded, gradient all-reduce
         from paper_2104_10013_b200.binding import DataParallelPINN
         prob = make_config("C2", method="pinn", weak=world, nx=1, ny=1,
                            n_f=16 * 15000 * world, n_u=960 * world)
-        dp = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=FLAG_TIMING)
+        dp = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=tflag)
         h = dp.h
         h_prob, local = h.prob, [0]
     elif args.workload in ("c3", "c4", "c5"):
@@ -272,13 +275,13 @@ def run_ours(args):
                            **({"gpus": 8} if args.workload == "c3" else {}))
         owner = lpt_owner([prob.n_points(q) for q in range(prob.n_sub)], world)
         local = [q for q in range(prob.n_sub) if owner[q] == rank]
-        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING)
+        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | tflag)
         h_prob = prob
     else:
         prob = make_config("C2", method=args.method, weak=world)
         owner = [s.ix // 4 for s in prob.subdomains]          # one 4x4 block per GPU
         local = [q for q in range(prob.n_sub) if owner[q] == rank]
-        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING)
+        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | tflag)
         h_prob = prob
     stream = h.stream
     pts_local = h.n_points
@@ -352,6 +355,24 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (K1, fused loss + grad)
     k1_flops, k2_flops = algorithmic_flops(h_prob, local)
     k1_ms = kt[1] / args.steps
+    k1_what = "K1 per launch (CUDA events inside the timed region)"
+    if world > 1:
+        # K1 (+ K5a) timed with events on the launching stream after the timed region
+        from paper_2104_10013_b200.binding import exchange_payload
+        ts = []
+        for _ in range(10):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            if args.method != "dp":
+                h.interface_payload()
+                exchange_payload(h.payload, h.table.plan, group)
+            e0.record(stream)
+            h.loss_grad(want_grad=False)
+            e1.record(stream)
+            ts.append((e0, e1))
+        torch.cuda.synchronize(dev)
+        k1_ms = sum(a.elapsed_time(b) for a, b in ts) / len(ts)
+        k1_what = "K1 + K5a per call, events on the launching stream after the timed region"
     peak_fp32 = 148 * 128 * 2 * 1965e6 / 1e12              # TFLOP/s, FP32 FMA pipe at clocks.max.sm
     achieved = k1_flops / (k1_ms * 1e-3) / 1e12
     traffic = None
@@ -363,14 +384,15 @@ def run_ours(args):
             traffic = None
 
     if rank == 0:
-        base_prob = (make_config("C2", method=args.method) if args.workload == "c2" else
-                     make_config(args.workload.upper(), method=args.method,
-                                 **({"gpus": 8} if args.workload == "c3" else {})))
-        base = (cpu_baseline(base_prob) if (world == 1 and not args.no_cpu and args.method != "dp") else None)
+        base = None
+        if world == 1 and not args.no_cpu and args.method != "dp":
+            base = cpu_baseline(make_config("C2", method=args.method) if args.workload == "c2" else
+                                make_config(args.workload.upper(), method=args.method,
+                                            **({"gpus": 8} if args.workload == "c3" else {})))
         acts = sorted({prob.act(q) for q in local})
         kname = (f"K1 k_fused<{prob.width},{prob.n_hidden},{prob.d_out},"
                  f"{'mixed' if len(acts) > 1 else acts[0]}> (fused fwd jets + loss + reverse)")
-        share = kt[1] / max(1e-9, sum(kt[:3]))
+        share = kt[1] / max(1e-9, sum(kt[:3])) if world == 1 else k1_ms / (t_max / args.steps)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
@@ -386,11 +408,12 @@ def run_ours(args):
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                          "frac": achieved / peak_fp32, "traffic": traffic,
                          "kernel": kname,
-                         "k1_ms_per_launch": k1_ms, "k1_gflop_per_launch": k1_flops / 1e9,
+                         "k1_ms_per_launch": k1_ms, "k1_timing": k1_what, "k1_gflop_per_launch": k1_flops / 1e9,
                          "k1_share_of_step": share,
                          "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md clocks.max.sm)"},
-            "kernels_ms_per_step": {"K2_payload": kt[0] / args.steps, "K1_loss_grad": k1_ms,
-                                    "K5_reduce_adam": kt[2] / args.steps},
+            "kernels_ms_per_step": {"K2_payload": kt[0] / args.steps if world == 1 else None,
+                                    "K1_loss_grad": k1_ms,
+                                    "K5_reduce_adam": kt[2] / args.steps if world == 1 else None},
             "gpu_launches": int(kt[3]),
             "clocks": clk,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
