@@ -96,22 +96,26 @@ __device__ __forceinline__ float comp(const float4& v, int m) {
   return m == 0 ? v.x : (m == 1 ? v.y : (m == 2 ? v.z : v.w));
 }
 
+// packed FP32 FMA (FFMA2, sm_100): acc.{xy,zw} += w * h.{xy,zw}.  Same
+// rounding as four fmaf calls; one issue slot per two FMAs.
+__device__ __forceinline__ void fma4(float4& acc, float w, const float4& h) {
+  const float2 ww = make_float2(w, w);
+  const float2 lo = __ffma2_rn(ww, make_float2(h.x, h.y), make_float2(acc.x, acc.y));
+  const float2 hi = __ffma2_rn(ww, make_float2(h.z, h.w), make_float2(acc.z, acc.w));
+  acc = make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
 // forward GEMM of one hidden layer for this thread's (point, neuron block):
-// z[c][jj] = sum_i W[j][i] Hin[i][p].c  (+ b on the value channel).
-// Per i-quad all 4*kJT accumulators are updated once per input component, so
+// z[jj].c = sum_i W[j][i] Hin[i][p].c  (+ b on the value channel).
+// Per i-quad all kJT jet accumulators are updated once per input component, so
 // consecutive FMAs are independent.
 template <int N, int NH, int DO>
 __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const float* __restrict__ W,
-                                         const float* __restrict__ b, float* z, int pg, int nb) {
+                                         const float* __restrict__ b, float4* z, int pg, int nb) {
   using C = KCfg<N, NH, DO>;
   const int j0 = nb * kJT;
 #pragma unroll
-  for (int jj = 0; jj < kJT; ++jj) {
-    z[jj] = b[j0 + jj];
-    z[kJT + jj] = 0.0f;
-    z[2 * kJT + jj] = 0.0f;
-    z[3 * kJT + jj] = 0.0f;
-  }
+  for (int jj = 0; jj < kJT; ++jj) z[jj] = make_float4(b[j0 + jj], 0.0f, 0.0f, 0.0f);
   const float* Wb = W + j0 * C::WS + nb * 4;
 #pragma unroll 2
   for (int i = 0; i < N; i += 4) {
@@ -124,25 +128,19 @@ __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const f
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
 #pragma unroll
-      for (int jj = 0; jj < kJT; ++jj) {
-        const float wm = comp(w[jj], m);
-        z[jj] = fmaf(wm, h[m].x, z[jj]);
-        z[kJT + jj] = fmaf(wm, h[m].y, z[kJT + jj]);
-        z[2 * kJT + jj] = fmaf(wm, h[m].z, z[2 * kJT + jj]);
-        z[3 * kJT + jj] = fmaf(wm, h[m].w, z[3 * kJT + jj]);
-      }
+      for (int jj = 0; jj < kJT; ++jj) fma4(z[jj], comp(w[jj], m), h[m]);
     }
   }
 }
 
-// reverse GEMM (input adjoint): hb[c][ii] = sum_j Zb[j][p].c W[j][j0 + ii]
+// reverse GEMM (input adjoint): hb[ii].c = sum_j Zb[j][p].c W[j][j0 + ii]
 template <int N, int NH, int DO>
-__device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const float* __restrict__ W, float* hb,
+__device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const float* __restrict__ W, float4* hb,
                                          int pg, int nb) {
   using C = KCfg<N, NH, DO>;
   const int j0 = nb * kJT;
 #pragma unroll
-  for (int e = 0; e < kA; ++e) hb[e] = 0.0f;
+  for (int e = 0; e < kJT; ++e) hb[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll 1
   for (int jb = 0; jb < C::NB; ++jb) {
     // rows jb*kJT .. +kJT-1 share the block skew jb*4
@@ -155,15 +153,8 @@ __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const fl
 #pragma unroll
       for (int q = 0; q < kJT / 2; ++q) {
         const float2 w = *reinterpret_cast<const float2*>(wr + 2 * q);
-        const float ws[2] = {w.x, w.y};
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-          const int ii = 2 * q + m;
-          hb[ii] = fmaf(zb.x, ws[m], hb[ii]);
-          hb[kJT + ii] = fmaf(zb.y, ws[m], hb[kJT + ii]);
-          hb[2 * kJT + ii] = fmaf(zb.z, ws[m], hb[2 * kJT + ii]);
-          hb[3 * kJT + ii] = fmaf(zb.w, ws[m], hb[3 * kJT + ii]);
-        }
+        fma4(hb[2 * q], w.x, zb);
+        fma4(hb[2 * q + 1], w.y, zb);
       }
     }
   }
@@ -183,13 +174,13 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
   if (tid < NBLK * S) {
     const int r = tid % NBLK, s = tid / NBLK;
     const int jb = r % NJ, ib = r / NJ;   // a warp covers 8 row blocks x 4 column blocks
-    float acc[JB][IB];
+    float2 acc2[JB][IB];   // (x.x + z.z, y.y + w.w) channel pairs, one FFMA2 each
     float db[JB];
 #pragma unroll
     for (int jj = 0; jj < JB; ++jj) {
       db[jj] = 0.0f;
 #pragma unroll
-      for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = 0.0f;
+      for (int ii = 0; ii < IB; ++ii) acc2[jj][ii] = make_float2(0.0f, 0.0f);
     }
 #pragma unroll 4
     for (int p = s * PS; p < (s + 1) * PS; ++p) {
@@ -199,14 +190,20 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) hr[ii] = H[(ib + NI * ii) * C::PSTR + p];
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
-        for (int jj = 0; jj < JB; ++jj)
-#pragma unroll
-          for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = fmaf(comp(zr[jj], m), comp(hr[ii], m), acc[jj][ii]);
+        for (int ii = 0; ii < IB; ++ii) {
+          acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].x, zr[jj].y), make_float2(hr[ii].x, hr[ii].y), acc2[jj][ii]);
+          acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].z, zr[jj].w), make_float2(hr[ii].z, hr[ii].w), acc2[jj][ii]);
+        }
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj) db[jj] += zr[jj].x;
     }
+    float acc[JB][IB];
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = acc2[jj][ii].x + acc2[jj][ii].y;
     if constexpr (S == 1) {
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj)
@@ -262,13 +259,6 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
       acc_add<DWS>(accB, jb + NJ * jj, v, first);
     }
   }
-}
-
-__device__ __forceinline__ float4 f4(const float* v, int jj) {
-  return make_float4(v[jj], v[kJT + jj], v[2 * kJT + jj], v[3 * kJT + jj]);
-}
-__device__ __forceinline__ void st4(float* v, int jj, float4 x) {
-  v[jj] = x.x; v[kJT + jj] = x.y; v[2 * kJT + jj] = x.z; v[3 * kJT + jj] = x.w;
 }
 
 // epilogue of one point (K2): u(x_I) and f.n (cPINN) or F (XPINN) into its
@@ -457,24 +447,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       cta_sync();
 
       // ------------------------------------------------------------ forward
-      float z[kA];
+      float4 z[kJT];   // this thread's neurons' jets (value, d1, d2, Delta_S)
       {
         const float x = sX[pg], y = sY[pg];
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) {
           const int j = j0 + jj;
           const float w0 = sW1[2 * j], w1 = sW1[2 * j + 1];
-          z[jj] = fmaf(w0, x, fmaf(w1, y, sB1[j]));   // z = W^1 x + b^1
-          z[kJT + jj] = w0;                           // dz/dx1 = W^1[:,0]
-          z[2 * kJT + jj] = w1;                       // dz/dx2 = W^1[:,1]
-          z[3 * kJT + jj] = 0.0f;                     // Delta z = 0
+          // z = W^1 x + b^1; dz/dx1 = W^1[:,0]; dz/dx2 = W^1[:,1]; Delta z = 0
+          z[jj] = make_float4(fmaf(w0, x, fmaf(w1, y, sB1[j])), w0, w1, 0.0f);
         }
         const float s = sSl[0];
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s, act);
-        if constexpr (MODE == 0) st.store(0, z);
+        for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<ACT>(z[jj].x, s, act);
+        if constexpr (MODE == 0) st.store(0, reinterpret_cast<const float*>(z));
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2, act);
+        for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(z[jj], s, m1, m2, act);
       }
       cta_sync();
 #pragma unroll 1
@@ -484,10 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         gemm_fwd<N, NH, DO>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
         const float s = sSl[k - 1];
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) z[jj] = stash_x<ACT>(z[jj], s, act);
-        if constexpr (MODE == 0) st.store(k - 1, z);
+        for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<ACT>(z[jj].x, s, act);
+        if constexpr (MODE == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
 #pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(f4(z, jj), s, m1, m2, act);
+        for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(z[jj], s, m1, m2, act);
         cta_sync();
       }
       const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
@@ -554,31 +542,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           for (int p = 0; p < C::P; ++p) acc += sU[p * DO + tid].x;
           acc_add<DSM>(A, LY::offB(NH + 1) + tid, acc, first);
         }
-        float hb[kA];
+        float4 hb[kJT];
 #pragma unroll
-        for (int e = 0; e < kA; ++e) hb[e] = 0.0f;
+        for (int e = 0; e < kJT; ++e) hb[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
         for (int o = 0; o < DO; ++o) {
           const float4 ub = sU[pg * DO + o];
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
-            const float w = sWo[o * C::WS + j0 + jj];
-            hb[jj] = fmaf(ub.x, w, hb[jj]);
-            hb[kJT + jj] = fmaf(ub.y, w, hb[kJT + jj]);
-            hb[2 * kJT + jj] = fmaf(ub.z, w, hb[2 * kJT + jj]);
-            hb[3 * kJT + jj] = fmaf(ub.w, w, hb[3 * kJT + jj]);
+            fma4(hb[jj], sWo[o * C::WS + j0 + jj], ub);
           }
         }
         {
-          st.load(NH - 1, z);
+          st.load(NH - 1, reinterpret_cast<float*>(z));
           const float s = sSl[NH - 1];
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, act));
+          for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<ACT>(z[jj], hb[jj], s, m1, m2, act);
           if (NH >= 2) {
-            st.load(NH - 2, z);
+            st.load(NH - 2, reinterpret_cast<float*>(z));
             const float s2 = sSl[NH - 2];
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2, act));
+            for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<ACT>(z[jj], s2, m1, m2, act);
           }
         }
         float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
@@ -586,8 +570,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         cta_sync();
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) {
-          bufZ[(j0 + jj) * C::PSTR + pg] = f4(hb, jj);
-          if (NH >= 2) bufH[(j0 + jj) * C::PSTR + pg] = f4(z, jj);
+          bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
+          if (NH >= 2) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
         }
         cta_sync();
 #pragma unroll 1
@@ -596,23 +580,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           gemm_dw<N, NH, DO, DSM>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
           // adjoint of H^{k-1}, then of Z^{k-1}
           gemm_bwd<N, NH, DO>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
-          st.load(k - 2, z);
+          st.load(k - 2, reinterpret_cast<float*>(z));
           const float s = sSl[k - 2];
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) st4(hb, jj, act_bwd<ACT>(f4(z, jj), f4(hb, jj), s, m1, m2, act));
+          for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<ACT>(z[jj], hb[jj], s, m1, m2, act);
           const bool more = (k - 1 >= 2);
           if (more) {
-            st.load(k - 3, z);
+            st.load(k - 3, reinterpret_cast<float*>(z));
             const float s2 = sSl[k - 3];
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) st4(z, jj, act_fwd<ACT>(f4(z, jj), s2, m1, m2, act));
+            for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<ACT>(z[jj], s2, m1, m2, act);
           }
           cta_sync();
           gemm_dw_reduce<N, NH, DO, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
-            bufZ[(j0 + jj) * C::PSTR + pg] = f4(hb, jj);
-            if (more) bufH[(j0 + jj) * C::PSTR + pg] = f4(z, jj);
+            bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
+            if (more) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
           }
           cta_sync();
         }
