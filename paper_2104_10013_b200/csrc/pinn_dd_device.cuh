@@ -18,11 +18,11 @@
 
 namespace pinn {
 
-constexpr int kThreads = 256;   // 8 warps: 2 per scheduler; warps w, w+4 share TMEM lane quarter w%4
+constexpr int kThreads = 256;   // default CTA: 8 warps, 2 per scheduler; warps w, w+4 share TMEM lane quarter w%4
 constexpr int kC = 4;           // jet channels
 constexpr int kJT = 10;         // neurons per thread (mapping A)
 constexpr int kA = kC * kJT;    // stash floats per thread per hidden layer
-constexpr int kStashCols = 256; // TMEM columns per thread (512 / 2 warps per lane quarter)
+constexpr int kStashCols = 256; // TMEM columns per thread (a 128-thread CTA allocates 256, a 256-thread CTA 512)
 
 __host__ __device__ constexpr int al4(int x) { return (x + 3) & ~3; }
 
@@ -67,13 +67,17 @@ constexpr bool lay_ok() {
 }
 
 // Kernel geometry for width N (mapping A: thread = (point group pg, neuron block nb)).
-template <int N, int NH, int DO>
+// T = threads per CTA: 256 (one CTA per SM) or 128 (two CTAs per SM, each
+// with its own barrier domain, so one CTA's barrier / latency-bound phases
+// overlap the other's GEMMs).
+template <int N, int NH, int DO, int T = kThreads>
 struct KCfg {
   static_assert(N % kJT == 0, "width must be a multiple of kJT");
   static_assert(lay_ok<N, NH, DO>(), "closed-form parameter layout mismatch");
   static_assert(NH * kA <= kStashCols, "reverse-mode stash exceeds the TMEM columns per thread");
   static constexpr int NB = N / kJT;           // neuron blocks
-  static constexpr int P = kThreads / NB;      // points per tile (1 point per thread)
+  static constexpr int P = T / NB;             // points per tile (1 point per thread)
+  static constexpr int CPS = 256 / T;          // CTAs per SM
   static constexpr int PSTR = P + 1;           // float4 row stride of activation buffers (odd)
   // W^k (k = 2..NH) rows: j*WS + (j/kJT)*4 floats (block skew against bank conflicts)
   static constexpr int WS = al4(N);
@@ -84,8 +88,9 @@ struct KCfg {
   static constexpr int NJ = N / JB;
   static constexpr int NI = N / IB;
   static constexpr int NBLK = NJ * NI;
-  static constexpr int S_MAX = kThreads / NBLK;
+  static constexpr int S_MAX = T / NBLK;
   static constexpr int S = S_MAX >= 16 ? 16 : (S_MAX >= 8 ? 8 : (S_MAX >= 4 ? 4 : (S_MAX >= 2 ? 2 : 1)));
+  static constexpr size_t SMEM_CAP = T == 256 ? 227 * 1024 : 113 * 1024;   // per CTA at CPS CTAs / SM
   static_assert(P % S == 0, "points per split");
   // smem carve (in floats)
   static constexpr int oW1 = 0;                            // [N][2]
@@ -104,11 +109,13 @@ struct KCfg {
   static constexpr int SCR = (S > 1) ? S * NBLK * JB * IB + S * NJ * JB : 0;
   static constexpr int oAcc = al4(oDw + SCR);              // per-chunk gradient accumulator
   static constexpr int ACC = Lay<N, NH, DO>::total();
-  static constexpr bool DW_SMEM = (size_t(al4(oAcc + ACC + 4)) * 4) <= 227 * 1024;
+  static constexpr bool DW_SMEM = (size_t(al4(oAcc + ACC + 4)) * 4) <= SMEM_CAP;
   static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 4);   // + tmem address slot
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
-  static_assert(SMEM <= 227 * 1024, "shared memory budget");
-  static_assert(NBLK * S <= kThreads, "dW blocks per CTA");
+  static_assert(SMEM <= SMEM_CAP, "shared memory budget");
+  static_assert(NBLK * S <= T, "dW blocks per CTA");
+  static_assert(T == 256 || T == 128, "128 or 256 threads per CTA");
+  static_assert(T == 256 || NH * kA <= kStashCols, "stash columns of a 128-thread CTA");
 
 };
 
@@ -225,12 +232,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(slot)));
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)), "n"(COLS));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
 }
-__device__ __forceinline__ void tmem_dealloc512(uint32_t taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(taddr));
+template <int COLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(COLS));
 }
 __device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -264,6 +273,7 @@ struct Stash {
   uint32_t taddr;     // TMEM address of this thread's column block
   float* g;           // global fallback base for this CTA (or nullptr)
   int tid;
+  int nthr;           // threads per CTA (global fallback stride)
   __device__ __forceinline__ void store(int slot, const float* v) {
     if (g == nullptr) {
       __syncwarp();   // tcgen05.st is .sync.aligned: the warp must be converged
@@ -272,7 +282,7 @@ struct Stash {
       tmem_wait_st();
     } else {
 #pragma unroll
-      for (int a = 0; a < kA; ++a) g[(size_t(slot) * kA + a) * kThreads + tid] = v[a];
+      for (int a = 0; a < kA; ++a) g[(size_t(slot) * kA + a) * nthr + tid] = v[a];
     }
   }
   __device__ __forceinline__ void load(int slot, float* v) {
@@ -282,7 +292,7 @@ struct Stash {
       for (int q = 0; q < kA / 8; ++q) tmem_ld8(taddr + slot * kA + q * 8, v + q * 8);
     } else {
 #pragma unroll
-      for (int a = 0; a < kA; ++a) v[a] = g[(size_t(slot) * kA + a) * kThreads + tid];
+      for (int a = 0; a < kA; ++a) v[a] = g[(size_t(slot) * kA + a) * nthr + tid];
     }
   }
 };

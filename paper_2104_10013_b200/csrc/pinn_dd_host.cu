@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -34,6 +35,8 @@ struct Ops {
   int pt;          // 1: point-per-thread kernel (narrow nets), 0: neuron-block kernel
   int pstride;     // Lay::total()
   int P;           // points per tile
+  int threads;     // threads per CTA of the fused kernels
+  int cps;         // CTAs per SM (persistent grid = cps x #SMs)
   size_t smem;     // dynamic smem of the fused kernel
   void (*k1)(const KArgs&, int grid, size_t smem, cudaStream_t);
   void (*k2)(const KArgs&, int grid, size_t smem, cudaStream_t);
@@ -44,27 +47,29 @@ struct Ops {
   cudaError_t (*setattr)(size_t);
 };
 
-template <int N, int NH, int DO, int ACT, bool PT = false>
+template <int N, int NH, int DO, int ACT, bool PT = false, int T = kThreads>
 struct Inst {
-  using C = KCfg<N, NH, DO>;
+  using C = KCfg<N, NH, DO, T>;
   using LY = Lay<N, NH, DO>;
   static size_t smem() {   // >= 120 KB forces 1 CTA / SM (the CTA owns all of TMEM)
     if constexpr (PT)
       return std::max<size_t>(PtCfg<N, NH, DO>::SMEM, 120 * 1024);
-    else
+    else if constexpr (T == 256)
       return std::max<size_t>(C::SMEM, 120 * 1024);
+    else
+      return C::SMEM;   // two 128-thread CTAs per SM, 256 TMEM columns each
   }
   static void k1(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
     if constexpr (PT)
       k_fused_pt<N, NH, DO, ACT, 0><<<grid, kPT, sm, s>>>(a);
     else
-      k_fused<N, NH, DO, ACT, 0><<<grid, kThreads, sm, s>>>(a);
+      k_fused<N, NH, DO, ACT, 0, T><<<grid, T, sm, s>>>(a);
   }
   static void k2(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
     if constexpr (PT)
       k_fused_pt<N, NH, DO, ACT, 1><<<grid, kPT, sm, s>>>(a);
     else
-      k_fused<N, NH, DO, ACT, 1><<<grid, kThreads, sm, s>>>(a);
+      k_fused<N, NH, DO, ACT, 1, T><<<grid, T, sm, s>>>(a);
   }
   static void pred(const float* params, int pstride, float sn, const float* pts, const int32_t* own, int64_t n,
                    float* out, const int32_t* sub_act, cudaStream_t s) {
@@ -101,16 +106,19 @@ struct Inst {
       if (e != cudaSuccess) return e;
       return cudaFuncSetAttribute(k_fused_pt<N, NH, DO, ACT, 1>, attr, int(sm));
     } else {
-      e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0>, attr, int(sm));
+      const auto carve = cudaFuncAttributePreferredSharedMemoryCarveout;
+      e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, attr, int(sm));
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, carve, 100);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, carve, 100);
       if (e != cudaSuccess) return e;
-      return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1>, attr, int(sm));
+      return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, attr, int(sm));
     }
   }
   static Ops ops() {
     static_assert(NH <= kMaxHidden, "too many hidden layers");
     if constexpr (PT) static_assert(PtCfg<N, NH, DO>::P == C::P, "both kernels tile by the same point count");
-    return Ops{N, NH, DO, ACT, PT ? 1 : 0, LY::total(), C::P, smem(), &k1, &k2, &pred, &packmap, &slopetab,
-               &setattr};
+    return Ops{N, NH, DO, ACT, PT ? 1 : 0, LY::total(), C::P, PT ? kPT : T, PT ? 1 : C::CPS, smem(), &k1, &k2,
+               &pred, &packmap, &slopetab, &setattr};
   }
 };
 
@@ -121,14 +129,24 @@ struct Inst {
 // on the B200).
 const Ops* find_ops(int N, int NH, int DO, int ACT, int pt = -1) {
   static const Ops table[] = {
-      Inst<20, 3, 1, 0, true>::ops(), Inst<20, 5, 1, 0, true>::ops(),
-      Inst<20, 3, 1, 0>::ops(),       Inst<20, 5, 1, 0>::ops(),
-      Inst<40, 6, 1, 0>::ops(),       Inst<80, 5, 3, 0>::ops(),
-      Inst<80, 3, 2, kActMixed>::ops(),
+      Inst<20, 3, 1, 0, true>::ops(),        Inst<20, 5, 1, 0, true>::ops(),
+      // width 20: two 128-thread CTAs per SM (C3 K1 0.369 -> 0.285 ms)
+      Inst<20, 3, 1, 0, false, 128>::ops(),  Inst<20, 5, 1, 0, false, 128>::ops(),
+      Inst<20, 3, 1, 0>::ops(),              Inst<20, 5, 1, 0>::ops(),
+      // widths 40 / 80: one 256-thread CTA per SM (the 128-thread 6x40 CTA is slower: 1.65 vs 1.55 ms)
+      Inst<40, 6, 1, 0>::ops(),              Inst<80, 5, 3, 0>::ops(),
+      Inst<80, 3, 2, kActMixed>::ops(),      Inst<40, 6, 1, 0, false, 128>::ops(),
   };
+  // development knob: PINN_DD_CTA_THREADS=128|256 picks the CTA size where both exist
+  const char* ev = std::getenv("PINN_DD_CTA_THREADS");
+  const int thr = ev ? std::atoi(ev) : 0;
+  const Ops* first = nullptr;
   for (const Ops& o : table)
-    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT && (pt < 0 || o.pt == pt)) return &o;
-  return nullptr;
+    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT && (pt < 0 || o.pt == pt)) {
+      if (!first) first = &o;
+      if (thr == 0 || o.pt || o.threads == thr) return &o;
+    }
+  return first;
 }
 
 }  // namespace
@@ -334,7 +352,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   const int nf = d->d_out + n_eq_of(d->pde);
   const size_t ns = size_t(d->n_sub);
   const size_t npt = size_t(d->n_points);
-  const int grid1 = std::min(n1, nsm);
+  const int grid1 = std::min(n1, nsm * ops->cps);
   Carve c;
   L->params = c.take<float>(ns * pstride);
   L->m = c.take<float>(ns * pstride);
@@ -362,7 +380,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->loss = c.take<float>(ns * 8);
   L->packmap = c.take<int32_t>(size_t(pstride));
   L->gstash = (d->flags & PINN_DD_FLAG_GLOBAL_STASH)
-                  ? c.take<float>(size_t(grid1) * d->n_hidden * kA * kThreads)
+                  ? c.take<float>(size_t(grid1) * d->n_hidden * kA * ops->threads)
                   : c.off;
   L->total = c.off;
   if (h) {
@@ -371,7 +389,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
     h->n_chunks1 = n1;
     h->n_chunks2 = n2;
     h->grid1 = grid1;
-    h->grid2 = std::max(1, std::min(n2, nsm));
+    h->grid2 = std::max(1, std::min(n2, nsm * ops->cps));
     h->pstride = pstride;
     h->nf = nf;
     h->neq = n_eq_of(d->pde);

@@ -16,6 +16,27 @@
 
 namespace pinn {
 
+// unroll factors of the GEMM loops (i-quads forward, 10-row blocks of the input
+// adjoint, points of dW); overridable at build time for variant sweeps
+#ifndef PINN_UF_FWD
+#define PINN_UF_FWD 10
+#endif
+#ifndef PINN_UF_BWD
+#define PINN_UF_BWD 1
+#endif
+#ifndef PINN_UF_DW
+#define PINN_UF_DW 8
+#endif
+// the per-subdomain-activation instance (three activation paths inlined) keeps
+// the short loops: fully unrolled it overflows the instruction cache (C5 K1
+// 0.59 -> 0.76 ms)
+template <int ACT>
+struct Uf {
+  static constexpr int fwd = ACT == 3 ? 2 : PINN_UF_FWD;
+  static constexpr int dw = ACT == 3 ? 4 : PINN_UF_DW;
+};
+constexpr int kUfBwd = PINN_UF_BWD;
+
 // CTA barrier preceded by an explicit warp reconvergence.
 __device__ __forceinline__ void cta_sync() {
   __syncwarp();
@@ -27,7 +48,7 @@ __device__ __forceinline__ void rmw_store(float* p, float v, bool first) {
 }
 
 // block-wide sum of R values per thread, fixed order (shuffle tree, then warps 0..3)
-template <int R, class T>
+template <int R, int NT, class T>
 __device__ __forceinline__ void block_sum(T* v, T* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -48,18 +69,18 @@ __device__ __forceinline__ void block_sum(T* v, T* red) {
     for (int r = 0; r < R; ++r) {
       T s = T(0);
 #pragma unroll
-      for (int ww = 0; ww < kThreads / 32; ++ww) s += red[ww * R + r];
+      for (int ww = 0; ww < NT / 32; ++ww) s += red[ww * R + r];
       v[r] = s;
     }
   }
 }
 
-template <int N, int NH, int DO>
+template <int N, int NH, int DO, int T>
 __device__ __forceinline__ void load_weights(const float* __restrict__ G, float slope_n, float* sm) {
-  using C = KCfg<N, NH, DO>;
+  using C = KCfg<N, NH, DO, T>;
   using LY = Lay<N, NH, DO>;
   const int tid = threadIdx.x;
-  for (int e = tid; e < 3 * N; e += kThreads) sm[C::oW1 + e] = G[LY::offW(1) + e];   // W^1 [N][2], b^1 (offB(1) = 2N)
+  for (int e = tid; e < 3 * N; e += T) sm[C::oW1 + e] = G[LY::offW(1) + e];   // W^1 [N][2], b^1 (offB(1) = 2N)
   static_assert(LY::offB(1) == 2 * N && C::oB1 == 2 * N, "W^1/b^1 contiguous");
   // hidden W^k rows: float4 copies; row j of layer k lands at j*WS + (j/kJT)*4
   constexpr int Q = N / 4;   // float4 per row
@@ -67,18 +88,18 @@ __device__ __forceinline__ void load_weights(const float* __restrict__ G, float 
   for (int k = 2; k <= NH; ++k) {
     const float4* W = reinterpret_cast<const float4*>(G + LY::offW(k));
     float* dst = sm + C::oWh + (k - 2) * C::WROWS;
-    for (int e = tid; e < N * Q; e += kThreads) {
+    for (int e = tid; e < N * Q; e += T) {
       const int j = e / Q, q = e - (e / Q) * Q;
       *reinterpret_cast<float4*>(dst + j * C::WS + (j / kJT) * 4 + 4 * q) = W[e];
     }
-    for (int e = tid; e < N; e += kThreads) sm[C::oBh + (k - 2) * N + e] = G[LY::offB(k) + e];
+    for (int e = tid; e < N; e += T) sm[C::oBh + (k - 2) * N + e] = G[LY::offB(k) + e];
   }
-  for (int e = tid; e < DO * N; e += kThreads) {
+  for (int e = tid; e < DO * N; e += T) {
     const int o = e / N, i = e - (e / N) * N;
     sm[C::oWo + o * C::WS + i] = G[LY::offW(NH + 1) + e];
   }
-  for (int e = tid; e < DO; e += kThreads) sm[C::oBo + e] = G[LY::offB(NH + 1) + e];
-  for (int e = tid; e < NH; e += kThreads) sm[C::oSl + e] = slope_n * G[LY::offA(e + 1)];
+  for (int e = tid; e < DO; e += T) sm[C::oBo + e] = G[LY::offB(NH + 1) + e];
+  for (int e = tid; e < NH; e += T) sm[C::oSl + e] = slope_n * G[LY::offA(e + 1)];
 }
 
 // gradient accumulator: shared memory for the whole chunk (DWS), else the
@@ -109,15 +130,15 @@ __device__ __forceinline__ void fma4(float4& acc, float w, const float4& h) {
 // z[jj].c = sum_i W[j][i] Hin[i][p].c  (+ b on the value channel).
 // Per i-quad all kJT jet accumulators are updated once per input component, so
 // consecutive FMAs are independent.
-template <int N, int NH, int DO>
+template <int N, int NH, int DO, int T, int UF>
 __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const float* __restrict__ W,
                                          const float* __restrict__ b, float4* z, int pg, int nb) {
-  using C = KCfg<N, NH, DO>;
+  using C = KCfg<N, NH, DO, T>;
   const int j0 = nb * kJT;
 #pragma unroll
   for (int jj = 0; jj < kJT; ++jj) z[jj] = make_float4(b[j0 + jj], 0.0f, 0.0f, 0.0f);
   const float* Wb = W + j0 * C::WS + nb * 4;
-#pragma unroll 2
+#pragma unroll UF
   for (int i = 0; i < N; i += 4) {
     float4 h[4];
 #pragma unroll
@@ -134,14 +155,14 @@ __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const f
 }
 
 // reverse GEMM (input adjoint): hb[ii].c = sum_j Zb[j][p].c W[j][j0 + ii]
-template <int N, int NH, int DO>
+template <int N, int NH, int DO, int T>
 __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const float* __restrict__ W, float4* hb,
                                          int pg, int nb) {
-  using C = KCfg<N, NH, DO>;
+  using C = KCfg<N, NH, DO, T>;
   const int j0 = nb * kJT;
 #pragma unroll
   for (int e = 0; e < kJT; ++e) hb[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll 1
+#pragma unroll kUfBwd
   for (int jb = 0; jb < C::NB; ++jb) {
     // rows jb*kJT .. +kJT-1 share the block skew jb*4
     const float* Wrow = W + jb * (kJT * C::WS + 4) + j0;
@@ -163,10 +184,10 @@ __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const fl
 // weight and bias gradient of one hidden layer (mapping B):
 // dW[j][i] += sum_p sum_c Zb[j][p].c H[i][p].c ;  db[j] += sum_p Zb[j][p].x
 // thread = (row block jb, column block ib, point split s); rows/cols interleaved.
-template <int N, int NH, int DO, bool DWS>
+template <int N, int NH, int DO, int T, bool DWS, int UF>
 __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const float4* __restrict__ H, float* accW,
                                         float* accB, bool first, float* sDw) {
-  using C = KCfg<N, NH, DO>;
+  using C = KCfg<N, NH, DO, T>;
   constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
   constexpr int PS = C::P / S;
   constexpr int DBOFF = S * NBLK * JB * IB;
@@ -182,7 +203,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc2[jj][ii] = make_float2(0.0f, 0.0f);
     }
-#pragma unroll 4
+#pragma unroll UF
     for (int p = s * PS; p < (s + 1) * PS; ++p) {
       float4 zr[JB], hr[IB];
 #pragma unroll
@@ -230,14 +251,45 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 // order into the accumulator.  Called after the CTA barrier that follows
 // gemm_bwd, so it needs no barrier of its own and its shared-memory latency
 // overlaps the activation-buffer stores that follow.
-template <int N, int NH, int DO, bool DWS>
+template <int N, int NH, int DO, int T, bool DWS>
 __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool first, const float* sDw) {
-  using C = KCfg<N, NH, DO>;
+  using C = KCfg<N, NH, DO, T>;
   constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
   constexpr int DBOFF = S * NBLK * JB * IB;
-  if constexpr (S > 1) {
+  if constexpr (S > 1 && !DWS) {
+    // global accumulator: thread e owns dW entries e, e + T, ... (coalesced),
+    // all loads of the chunk partial issued before any store (one L2 round trip)
     const int tid = threadIdx.x;
-    for (int e = tid; e < NBLK * JB; e += kThreads) {   // (block, row) items; IB columns each
+    constexpr int NE = N * N, IT = (NE + T - 1) / T;
+    float v[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      if (e < NE) {
+        const int j = e / N, i = e - (e / N) * N;
+        const int r = (j % NJ) + NJ * (i % NI);
+        const float* src = sDw + r * JB * IB + (j / NJ) * IB + (i / NI);
+        float x = src[0];
+#pragma unroll
+        for (int s = 1; s < S; ++s) x += src[s * NBLK * JB * IB];
+        v[it] = first ? x : accW[e] + x;
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      if (e < NE) accW[e] = v[it];
+    }
+    if (tid < N) {
+      const int jb = tid % NJ, jj = tid / NJ;
+      float x = 0.0f;
+#pragma unroll
+      for (int s = 0; s < S; ++s) x += sDw[DBOFF + (s * NJ + jb) * JB + jj];
+      accB[tid] = first ? x : accB[tid] + x;
+    }
+  } else if constexpr (S > 1) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < NBLK * JB; e += T) {   // (block, row) items; IB columns each
       const int r = e / JB, jj = e - (e / JB) * JB;
       const int jb = r % NJ, ib = r / NJ;
       const float* src = sDw + r * JB * IB + jj * IB;
@@ -251,7 +303,7 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v[ii], first);
     }
-    for (int e = tid; e < NJ * JB; e += kThreads) {
+    for (int e = tid; e < NJ * JB; e += T) {
       const int jb = e / JB, jj = e % JB;
       float v = 0.0f;
 #pragma unroll
@@ -347,9 +399,9 @@ __device__ __forceinline__ void point_adjoint(const KArgs& a, int64_t gp, float 
   }
 }
 
-template <int N, int NH, int DO, int ACT, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
-  using C = KCfg<N, NH, DO>;
+template <int N, int NH, int DO, int ACT, int MODE, int T>
+__global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
+  using C = KCfg<N, NH, DO, T>;
   using LY = Lay<N, NH, DO>;
   extern __shared__ __align__(16) float sm[];
   const int tid = threadIdx.x;
@@ -376,13 +428,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 
   Stash st;
   st.tid = tid;
+  st.nthr = T;
   st.g = nullptr;
   st.taddr = 0;
   if constexpr (MODE == 0) {
     if (a.gstash == nullptr) {
       if (tid < 32) {
         __syncwarp();
-        tmem_alloc512(tslot);
+        tmem_alloc<2 * T>(tslot);
       }
       tmem_fence_before();
       cta_sync();
@@ -390,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       const int warp = tid >> 5;
       st.taddr = *tslot + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * kStashCols);
     } else {
-      st.g = a.gstash + size_t(blockIdx.x) * NH * kA * kThreads;
+      st.g = a.gstash + size_t(blockIdx.x) * NH * kA * T;
     }
   }
 
@@ -410,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
     const Chunk ch = a.chunks[c];
     if (ch.sub != cur_sub) {
       cta_sync();
-      load_weights<N, NH, DO>(a.params + size_t(ch.sub) * a.pstride, a.slope_n, sm);
+      load_weights<N, NH, DO, T>(a.params + size_t(ch.sub) * a.pstride, a.slope_n, sm);
       cur_sub = ch.sub;
     }
     const float4 lw = a.sub_w[ch.sub];
@@ -419,13 +472,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
     float* A = DSM ? sAcc : Pc;   // gradient accumulator of this chunk
     if constexpr (MODE == 0 && DSM) {
       cta_sync();
-      for (int e = tid; e < C::ACC; e += kThreads) sAcc[e] = 0.0f;
+      for (int e = tid; e < C::ACC; e += T) sAcc[e] = 0.0f;
     }
     const int ntiles = (ch.count + C::P - 1) / C::P;
     if constexpr (MODE == 0) {
       if (ntiles == 0) {   // a subdomain without points: its slot holds zeros
         if (!DSM)
-          for (int e = tid; e < a.pstride; e += kThreads) Pc[e] = 0.0f;
+          for (int e = tid; e < a.pstride; e += T) Pc[e] = 0.0f;
         if (tid < 4) a.partial_loss[size_t(c) * 4 + tid] = 0.0f;
       }
     }
@@ -435,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       const int np = min(C::P, ch.count - t * C::P);
       const bool first = (t == 0);
       cta_sync();
-      for (int p = tid; p < C::P; p += kThreads) {
+      for (int p = tid; p < C::P; p += T) {
         float x = 0.0f, y = 0.0f;
         if (p < np) {
           x = a.coords[p0 + p];
@@ -469,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       for (int k = 2; k <= NH; ++k) {
         const float4* Hin = (k & 1) ? buf1 : buf0;
         float4* Hout = (k & 1) ? buf0 : buf1;
-        gemm_fwd<N, NH, DO>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
+        gemm_fwd<N, NH, DO, T, Uf<ACT>::fwd>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
         const float s = sSl[k - 1];
 #pragma unroll
         for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<ACT>(z[jj].x, s, act);
@@ -479,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         cta_sync();
       }
       const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
-      for (int idx = tid; idx < C::P * DO; idx += kThreads) {
+      for (int idx = tid; idx < C::P * DO; idx += T) {
         const int p = idx % C::P, o = idx / C::P;
         float4 acc = make_float4(sBo[o], 0.0f, 0.0f, 0.0f);
         const float* w = sWo + o * C::WS;
@@ -499,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       // ----------------------------------------------------------- epilogue
       if constexpr (MODE == 1) {
         // payload: u(x_I) and f.n (cPINN) or F (XPINN) (Algorithm 1)
-        for (int p = tid; p < np; p += kThreads) {
+        for (int p = tid; p < np; p += T) {
           float4 U[DO];
 #pragma unroll
           for (int o = 0; o < DO; ++o) U[o] = sU[p * DO + o];
@@ -508,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         continue;
       } else {
         float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // MSE_u, MSE_F, MSE_uavg, MSE_if partials
-        for (int p = tid; p < C::P; p += kThreads) {
+        for (int p = tid; p < C::P; p += T) {
           float4 U[DO], Ub[DO];
 #pragma unroll
           for (int o = 0; o < DO; ++o) {
@@ -523,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 
         // ------------------------------------------------------------ reverse
         // output layer: dW^L, db^L
-        for (int t4 = tid; t4 < 4 * DO * N; t4 += kThreads) {   // warp-uniform trip count
+        for (int t4 = tid; t4 < 4 * DO * N; t4 += T) {   // warp-uniform trip count
           const int qq = t4 & 3, idx = t4 >> 2;
           const int o = idx / N, i = idx % N;
           float acc = 0.0f;
@@ -577,9 +630,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
 #pragma unroll 1
         for (int k = NH; k >= 2; --k) {
           // dW^k, db^k
-          gemm_dw<N, NH, DO, DSM>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
+          gemm_dw<N, NH, DO, T, DSM, Uf<ACT>::dw>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
           // adjoint of H^{k-1}, then of Z^{k-1}
-          gemm_bwd<N, NH, DO>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
+          gemm_bwd<N, NH, DO, T>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
           st.load(k - 2, reinterpret_cast<float*>(z));
           const float s = sSl[k - 2];
 #pragma unroll
@@ -592,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
             for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<ACT>(z[jj], s2, m1, m2, act);
           }
           cta_sync();
-          gemm_dw_reduce<N, NH, DO, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
+          gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
             bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
@@ -601,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
           cta_sync();
         }
         // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
-        for (int t4 = tid; t4 < 4 * N; t4 += kThreads) {
+        for (int t4 = tid; t4 < 4 * N; t4 += T) {
           const int qq = t4 & 3, j = t4 >> 2;
           float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
 #pragma unroll 4
@@ -628,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
         float red[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) red[r] = lsum[r];
-        block_sum<4>(red, sRed);
+        block_sum<4, T>(red, sRed);
         if (tid == 0) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) rmw_store(a.partial_loss + size_t(c) * 4 + r, red[r], first);
@@ -642,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
     if constexpr (MODE == 0 && DSM) {
       // flush the chunk's gradient (slope slots stay 0; K5 fills them)
       cta_sync();
-      for (int e = tid; e < C::ACC; e += kThreads) Pc[e] = sAcc[e];
+      for (int e = tid; e < C::ACC; e += T) Pc[e] = sAcc[e];
     }
     cta_sync();   // every thread has read s_next before it is overwritten
   }
@@ -661,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused(const KArgs a) {
       tmem_fence_after();
       if (tid < 32) {
         __syncwarp();
-        tmem_dealloc512(*tslot);
+        tmem_dealloc<2 * T>(*tslot);
       }
     }
   }

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kPT, 1) k_fused_pt(const KArgs a) {
     if (a.gstash == nullptr) {
       if (tid < 32) {
         __syncwarp();
-        tmem_alloc512(tslot);
+        tmem_alloc<512>(tslot);
       }
       tmem_fence_before();
       cta_sync();
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kPT, 1) k_fused_pt(const KArgs a) {
       tmem_fence_after();
       if (tid < 32) {
         __syncwarp();
-        tmem_dealloc512(*tslot);
+        tmem_dealloc<512>(*tslot);
       }
     }
   }
