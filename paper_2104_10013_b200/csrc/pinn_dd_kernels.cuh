@@ -482,20 +482,29 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         if (tid < 4) a.partial_loss[size_t(c) * 4 + tid] = 0.0f;
       }
     }
+    // coordinates of the next tile are loaded into registers while the
+    // current tile computes (thread p < P owns point p of a tile)
+    static_assert(C::P <= T, "one staged point per thread");
+    float cx = 0.0f, cy = 0.0f;
+    if (tid < min(C::P, ch.count)) {
+      cx = a.coords[int64_t(ch.start) + tid];
+      cy = a.coords[a.n_points + int64_t(ch.start) + tid];
+    }
+    float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // this thread's MSE_u, MSE_F, MSE_uavg, MSE_if partials (chunk)
 #pragma unroll 1
     for (int t = 0; t < ntiles; ++t) {
       const int64_t p0 = int64_t(ch.start) + int64_t(t) * C::P;
       const int np = min(C::P, ch.count - t * C::P);
       const bool first = (t == 0);
       cta_sync();
-      for (int p = tid; p < C::P; p += T) {
-        float x = 0.0f, y = 0.0f;
-        if (p < np) {
-          x = a.coords[p0 + p];
-          y = a.coords[a.n_points + p0 + p];
+      if (tid < C::P) {
+        sX[tid] = cx;
+        sY[tid] = cy;
+        cx = cy = 0.0f;
+        if (t + 1 < ntiles && tid < min(C::P, ch.count - (t + 1) * C::P)) {
+          cx = a.coords[p0 + C::P + tid];
+          cy = a.coords[a.n_points + p0 + C::P + tid];
         }
-        sX[p] = x;
-        sY[p] = y;
       }
       cta_sync();
 
@@ -560,7 +569,6 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         }
         continue;
       } else {
-        float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // MSE_u, MSE_F, MSE_uavg, MSE_if partials
         for (int p = tid; p < C::P; p += T) {
           float4 U[DO], Ub[DO];
 #pragma unroll
@@ -677,18 +685,20 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             acc_add<DSM>(A, LY::offB(1) + j, ab, first);
           }
         }
-        // loss partials; the slope entries of the partial stay 0 (K5 fills them)
-        float red[4];
+        // the slope entries of the partial stay 0 (K5 fills them)
+        if (tid == 0 && first && !DSM) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) red[r] = lsum[r];
-        block_sum<4, T>(red, sRed);
+          for (int k = 1; k <= NH; ++k) Pc[LY::offA(k)] = 0.0f;
+        }
+      }
+    }
+    if constexpr (MODE == 0) {
+      // loss partials of the chunk: fixed-order block reduction once per chunk
+      if (ntiles > 0) {
+        block_sum<4, T>(lsum, sRed);
         if (tid == 0) {
 #pragma unroll
-          for (int r = 0; r < 4; ++r) rmw_store(a.partial_loss + size_t(c) * 4 + r, red[r], first);
-          if (first && !DSM) {
-#pragma unroll
-            for (int k = 1; k <= NH; ++k) Pc[LY::offA(k)] = 0.0f;
-          }
+          for (int r = 0; r < 4; ++r) a.partial_loss[size_t(c) * 4 + r] = lsum[r];
         }
       }
     }
