@@ -375,11 +375,15 @@ def run_ours(args):
         k1_what = "K1 + K5a per call, events on the launching stream after the timed region"
     peak_fp32 = 148 * 128 * 2 * 1965e6 / 1e12              # TFLOP/s, FP32 FMA pipe at clocks.max.sm
     achieved = k1_flops / (k1_ms * 1e-3) / 1e12
+    # DRAM bytes per K1 launch of THIS workload from one committed ncu --set full
+    # capture (tools/dram_table.py); null when no capture of this workload exists
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_dram_bytes.json")
+    wl_key = f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}"
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            ent = json.load(open(prof)).get(wl_key)
+            traffic = ent.get("dram_bytes_per_launch") if ent else None
         except Exception:
             traffic = None
 

@@ -288,27 +288,37 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
       accB[tid] = first ? x : accB[tid] + x;
     }
   } else if constexpr (S > 1) {
+    // shared accumulator: entry e = (block r, row jj, column ii) of the split
+    // scratch is contiguous in e, so thread e's S loads are conflict-free; all
+    // loads are issued before any store (one shared-memory round trip)
     const int tid = threadIdx.x;
-    for (int e = tid; e < NBLK * JB; e += T) {   // (block, row) items; IB columns each
-      const int r = e / JB, jj = e - (e / JB) * JB;
-      const int jb = r % NJ, ib = r / NJ;
-      const float* src = sDw + r * JB * IB + jj * IB;
-      float v[IB];
+    constexpr int NE = NBLK * JB * IB, IT = (NE + T - 1) / T;
+    float v[IT];
+    int off[IT];
 #pragma unroll
-      for (int ii = 0; ii < IB; ++ii) v[ii] = src[ii];
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      if (e < NE) {
+        float x = sDw[e];
 #pragma unroll
-      for (int s = 1; s < S; ++s)
-#pragma unroll
-        for (int ii = 0; ii < IB; ++ii) v[ii] += src[s * NBLK * JB * IB + ii];
-#pragma unroll
-      for (int ii = 0; ii < IB; ++ii) acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, v[ii], first);
+        for (int s = 1; s < S; ++s) x += sDw[s * NE + e];
+        const int r = e / (JB * IB), rem = e - r * (JB * IB);
+        const int jj = rem / IB, ii = rem - jj * IB;
+        off[it] = ((r % NJ) + NJ * jj) * N + (r / NJ) + NI * ii;
+        v[it] = x;
+      }
     }
-    for (int e = tid; e < NJ * JB; e += T) {
-      const int jb = e / JB, jj = e % JB;
-      float v = 0.0f;
 #pragma unroll
-      for (int s = 0; s < S; ++s) v += sDw[DBOFF + (s * NJ + jb) * JB + jj];
-      acc_add<DWS>(accB, jb + NJ * jj, v, first);
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      if (e < NE) acc_add<DWS>(accW, off[it], v[it], first);
+    }
+    if (tid < N) {
+      const int jb = tid % NJ, jj = tid / NJ;
+      float x = 0.0f;
+#pragma unroll
+      for (int s = 0; s < S; ++s) x += sDw[DBOFF + (s * NJ + jb) * JB + jj];
+      acc_add<DWS>(accB, tid, x, first);
     }
   }
 }
