@@ -12,6 +12,8 @@
 // K6  k_predict: value-only forward + Eq. (4) stitching.
 #pragma once
 
+#include <type_traits>
+
 #include "pinn_dd_device.cuh"
 
 namespace pinn {
@@ -27,14 +29,7 @@ namespace pinn {
 #ifndef PINN_UF_DW
 #define PINN_UF_DW 8
 #endif
-// the per-subdomain-activation instance (three activation paths inlined) keeps
-// the short loops: fully unrolled it overflows the instruction cache (C5 K1
-// 0.59 -> 0.76 ms)
-template <int ACT>
-struct Uf {
-  static constexpr int fwd = ACT == 3 ? 2 : PINN_UF_FWD;
-  static constexpr int dw = ACT == 3 ? 4 : PINN_UF_DW;
-};
+constexpr int kUfFwd = PINN_UF_FWD, kUfDw = PINN_UF_DW;
 constexpr int kUfBwd = PINN_UF_BWD;
 
 // CTA barrier preceded by an explicit warp reconvergence.
@@ -492,225 +487,241 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         if (tid < 4) a.partial_loss[size_t(c) * 4 + tid] = 0.0f;
       }
     }
-    // coordinates of the next tile are loaded into registers while the
-    // current tile computes (thread p < P owns point p of a tile)
-    static_assert(C::P <= T, "one staged point per thread");
-    float cx = 0.0f, cy = 0.0f;
-    if (tid < min(C::P, ch.count)) {
-      cx = a.coords[int64_t(ch.start) + tid];
-      cy = a.coords[a.n_points + int64_t(ch.start) + tid];
-    }
-    float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // this thread's MSE_u, MSE_F, MSE_uavg, MSE_if partials (chunk)
-#pragma unroll 1
-    for (int t = 0; t < ntiles; ++t) {
-      const int64_t p0 = int64_t(ch.start) + int64_t(t) * C::P;
-      const int np = min(C::P, ch.count - t * C::P);
-      const bool first = (t == 0);
-      cta_sync();
-      if (tid < C::P) {
-        sX[tid] = cx;
-        sY[tid] = cy;
-        cx = cy = 0.0f;
-        if (t + 1 < ntiles && tid < min(C::P, ch.count - (t + 1) * C::P)) {
-          cx = a.coords[p0 + C::P + tid];
-          cy = a.coords[a.n_points + p0 + C::P + tid];
-        }
+    // the chunk's tiles, compiled once per activation: the per-subdomain-activation
+    // instance dispatches here per chunk, so each hot loop holds one activation
+    // path only (three inlined paths overflowed the instruction cache)
+    auto chunk_body = [&](auto act_c) {
+      constexpr int AS = decltype(act_c)::value;
+      // coordinates of the next tile are loaded into registers while the
+      // current tile computes (thread p < P owns point p of a tile)
+      static_assert(C::P <= T, "one staged point per thread");
+      float cx = 0.0f, cy = 0.0f;
+      if (tid < min(C::P, ch.count)) {
+        cx = a.coords[int64_t(ch.start) + tid];
+        cy = a.coords[a.n_points + int64_t(ch.start) + tid];
       }
-      cta_sync();
-
-      // ------------------------------------------------------------ forward
-      float4 z[kJT];   // this thread's neurons' jets (value, d1, d2, Delta_S)
-      {
-        const float x = sX[pg], y = sY[pg];
-#pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) {
-          const int j = j0 + jj;
-          const float w0 = sW1[2 * j], w1 = sW1[2 * j + 1];
-          // z = W^1 x + b^1; dz/dx1 = W^1[:,0]; dz/dx2 = W^1[:,1]; Delta z = 0
-          z[jj] = make_float4(fmaf(w0, x, fmaf(w1, y, sB1[j])), w0, w1, 0.0f);
-        }
-        const float s = sSl[0];
-#pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<ACT>(z[jj].x, s, act);
-        if constexpr (MODE == 0) st.store(0, reinterpret_cast<const float*>(z));
-#pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(z[jj], s, m1, m2, act);
-      }
-      cta_sync();
+      float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // this thread's MSE_u, MSE_F, MSE_uavg, MSE_if partials (chunk)
 #pragma unroll 1
-      for (int k = 2; k <= NH; ++k) {
-        const float4* Hin = (k & 1) ? buf1 : buf0;
-        float4* Hout = (k & 1) ? buf0 : buf1;
-        gemm_fwd<N, NH, DO, T, Uf<ACT>::fwd>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
-        const float s = sSl[k - 1];
-#pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<ACT>(z[jj].x, s, act);
-        if constexpr (MODE == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
-#pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<ACT>(z[jj], s, m1, m2, act);
+      for (int t = 0; t < ntiles; ++t) {
+        const int64_t p0 = int64_t(ch.start) + int64_t(t) * C::P;
+        const int np = min(C::P, ch.count - t * C::P);
+        const bool first = (t == 0);
         cta_sync();
-      }
-      const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
-      for (int idx = tid; idx < C::P * DO; idx += T) {
-        const int p = idx % C::P, o = idx / C::P;
-        float4 acc = make_float4(sBo[o], 0.0f, 0.0f, 0.0f);
-        const float* w = sWo + o * C::WS;
-#pragma unroll 4
-        for (int i = 0; i < N; ++i) {
-          const float4 h = HL[i * C::PSTR + p];
-          const float wi = w[i];
-          acc.x = fmaf(wi, h.x, acc.x);
-          acc.y = fmaf(wi, h.y, acc.y);
-          acc.z = fmaf(wi, h.z, acc.z);
-          acc.w = fmaf(wi, h.w, acc.w);
-        }
-        sU[p * DO + o] = acc;
-      }
-      cta_sync();
-
-      // ----------------------------------------------------------- epilogue
-      if constexpr (MODE == 1) {
-        // payload: u(x_I) and f.n (cPINN) or F (XPINN) (Algorithm 1)
-        for (int p = tid; p < np; p += T) {
-          float4 U[DO];
-#pragma unroll
-          for (int o = 0; o < DO; ++o) U[o] = sU[p * DO + o];
-          point_payload<DO>(a, p0 + p, sX[p], sY[p], U);
-        }
-        continue;
-      } else {
-        for (int p = tid; p < C::P; p += T) {
-          float4 U[DO], Ub[DO];
-#pragma unroll
-          for (int o = 0; o < DO; ++o) {
-            U[o] = sU[p * DO + o];
-            Ub[o] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (tid < C::P) {
+          sX[tid] = cx;
+          sY[tid] = cy;
+          cx = cy = 0.0f;
+          if (t + 1 < ntiles && tid < min(C::P, ch.count - (t + 1) * C::P)) {
+            cx = a.coords[p0 + C::P + tid];
+            cy = a.coords[a.n_points + p0 + C::P + tid];
           }
-          if (p < np) point_adjoint<DO>(a, p0 + p, sX[p], sY[p], lw, U, Ub, lsum);
-#pragma unroll
-          for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
         }
         cta_sync();
 
-        // ------------------------------------------------------------ reverse
-        // output layer: dW^L, db^L
-        for (int t4 = tid; t4 < 4 * DO * N; t4 += T) {   // warp-uniform trip count
-          const int qq = t4 & 3, idx = t4 >> 2;
-          const int o = idx / N, i = idx % N;
-          float acc = 0.0f;
-#pragma unroll 4
-          for (int p = qq; p < C::P; p += 4) {
-            const float4 h = HL[i * C::PSTR + p];
-            const float4 ub = sU[p * DO + o];
-            acc = fmaf(h.x, ub.x, fmaf(h.y, ub.y, fmaf(h.z, ub.z, fmaf(h.w, ub.w, acc))));
-          }
-          acc += __shfl_xor_sync(__activemask(), acc, 1);
-          acc += __shfl_xor_sync(__activemask(), acc, 2);
-          if (qq == 0) acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
-        }
-        if (tid < DO) {
-          float acc = 0.0f;
-          for (int p = 0; p < C::P; ++p) acc += sU[p * DO + tid].x;
-          acc_add<DSM>(A, LY::offB(NH + 1) + tid, acc, first);
-        }
-        float4 hb[kJT];
-#pragma unroll
-        for (int e = 0; e < kJT; ++e) hb[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll
-        for (int o = 0; o < DO; ++o) {
-          const float4 ub = sU[pg * DO + o];
+        // ------------------------------------------------------------ forward
+        float4 z[kJT];   // this thread's neurons' jets (value, d1, d2, Delta_S)
+        {
+          const float x = sX[pg], y = sY[pg];
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
-            fma4(hb[jj], sWo[o * C::WS + j0 + jj], ub);
+            const int j = j0 + jj;
+            const float w0 = sW1[2 * j], w1 = sW1[2 * j + 1];
+            // z = W^1 x + b^1; dz/dx1 = W^1[:,0]; dz/dx2 = W^1[:,1]; Delta z = 0
+            z[jj] = make_float4(fmaf(w0, x, fmaf(w1, y, sB1[j])), w0, w1, 0.0f);
           }
-        }
-        {
-          st.load(NH - 1, reinterpret_cast<float*>(z));
-          const float s = sSl[NH - 1];
+          const float s = sSl[0];
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<ACT>(z[jj], hb[jj], s, m1, m2, act);
-          if (NH >= 2) {
-            st.load(NH - 2, reinterpret_cast<float*>(z));
-            const float s2 = sSl[NH - 2];
+          for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
+          if constexpr (MODE == 0) st.store(0, reinterpret_cast<const float*>(z));
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<ACT>(z[jj], s2, m1, m2, act);
-          }
-        }
-        float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
-        float4* bufH = buf1;   // activation of the layer below
-        cta_sync();
-#pragma unroll
-        for (int jj = 0; jj < kJT; ++jj) {
-          bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
-          if (NH >= 2) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
+          for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
         }
         cta_sync();
 #pragma unroll 1
-        for (int k = NH; k >= 2; --k) {
-          // dW^k, db^k
-          gemm_dw<N, NH, DO, T, DSM, Uf<ACT>::dw>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
-          // adjoint of H^{k-1}, then of Z^{k-1}
-          gemm_bwd<N, NH, DO, T>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
-          st.load(k - 2, reinterpret_cast<float*>(z));
-          const float s = sSl[k - 2];
+        for (int k = 2; k <= NH; ++k) {
+          const float4* Hin = (k & 1) ? buf1 : buf0;
+          float4* Hout = (k & 1) ? buf0 : buf1;
+          gemm_fwd<N, NH, DO, T, kUfFwd>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
+          const float s = sSl[k - 1];
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<ACT>(z[jj], hb[jj], s, m1, m2, act);
-          const bool more = (k - 1 >= 2);
-          if (more) {
-            st.load(k - 3, reinterpret_cast<float*>(z));
-            const float s2 = sSl[k - 3];
+          for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
+          if constexpr (MODE == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<ACT>(z[jj], s2, m1, m2, act);
+          for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
+          cta_sync();
+        }
+        const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
+        for (int idx = tid; idx < C::P * DO; idx += T) {
+          const int p = idx % C::P, o = idx / C::P;
+          float4 acc = make_float4(sBo[o], 0.0f, 0.0f, 0.0f);
+          const float* w = sWo + o * C::WS;
+#pragma unroll 4
+          for (int i = 0; i < N; ++i) {
+            const float4 h = HL[i * C::PSTR + p];
+            const float wi = w[i];
+            acc.x = fmaf(wi, h.x, acc.x);
+            acc.y = fmaf(wi, h.y, acc.y);
+            acc.z = fmaf(wi, h.z, acc.z);
+            acc.w = fmaf(wi, h.w, acc.w);
+          }
+          sU[p * DO + o] = acc;
+        }
+        cta_sync();
+
+        // ----------------------------------------------------------- epilogue
+        if constexpr (MODE == 1) {
+          // payload: u(x_I) and f.n (cPINN) or F (XPINN) (Algorithm 1)
+          for (int p = tid; p < np; p += T) {
+            float4 U[DO];
+#pragma unroll
+            for (int o = 0; o < DO; ++o) U[o] = sU[p * DO + o];
+            point_payload<DO>(a, p0 + p, sX[p], sY[p], U);
+          }
+          continue;
+        } else {
+          for (int p = tid; p < C::P; p += T) {
+            float4 U[DO], Ub[DO];
+#pragma unroll
+            for (int o = 0; o < DO; ++o) {
+              U[o] = sU[p * DO + o];
+              Ub[o] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
+            if (p < np) point_adjoint<DO>(a, p0 + p, sX[p], sY[p], lw, U, Ub, lsum);
+#pragma unroll
+            for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
           }
           cta_sync();
-          gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
+
+          // ------------------------------------------------------------ reverse
+          // output layer: dW^L, db^L
+          for (int t4 = tid; t4 < 4 * DO * N; t4 += T) {   // warp-uniform trip count
+            const int qq = t4 & 3, idx = t4 >> 2;
+            const int o = idx / N, i = idx % N;
+            float acc = 0.0f;
+#pragma unroll 4
+            for (int p = qq; p < C::P; p += 4) {
+              const float4 h = HL[i * C::PSTR + p];
+              const float4 ub = sU[p * DO + o];
+              acc = fmaf(h.x, ub.x, fmaf(h.y, ub.y, fmaf(h.z, ub.z, fmaf(h.w, ub.w, acc))));
+            }
+            acc += __shfl_xor_sync(__activemask(), acc, 1);
+            acc += __shfl_xor_sync(__activemask(), acc, 2);
+            if (qq == 0) acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
+          }
+          if (tid < DO) {
+            float acc = 0.0f;
+            for (int p = 0; p < C::P; ++p) acc += sU[p * DO + tid].x;
+            acc_add<DSM>(A, LY::offB(NH + 1) + tid, acc, first);
+          }
+          float4 hb[kJT];
+#pragma unroll
+          for (int e = 0; e < kJT; ++e) hb[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+          for (int o = 0; o < DO; ++o) {
+            const float4 ub = sU[pg * DO + o];
+#pragma unroll
+            for (int jj = 0; jj < kJT; ++jj) {
+              fma4(hb[jj], sWo[o * C::WS + j0 + jj], ub);
+            }
+          }
+          {
+            st.load(NH - 1, reinterpret_cast<float*>(z));
+            const float s = sSl[NH - 1];
+#pragma unroll
+            for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+            if (NH >= 2) {
+              st.load(NH - 2, reinterpret_cast<float*>(z));
+              const float s2 = sSl[NH - 2];
+#pragma unroll
+              for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+            }
+          }
+          float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
+          float4* bufH = buf1;   // activation of the layer below
+          cta_sync();
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
             bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
-            if (more) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
+            if (NH >= 2) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
           }
           cta_sync();
-        }
-        // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
-        for (int t4 = tid; t4 < 4 * N; t4 += T) {
-          const int qq = t4 & 3, j = t4 >> 2;
-          float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
+#pragma unroll 1
+          for (int k = NH; k >= 2; --k) {
+            // dW^k, db^k
+            gemm_dw<N, NH, DO, T, DSM, kUfDw>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
+            // adjoint of H^{k-1}, then of Z^{k-1}
+            gemm_bwd<N, NH, DO, T>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
+            st.load(k - 2, reinterpret_cast<float*>(z));
+            const float s = sSl[k - 2];
+#pragma unroll
+            for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+            const bool more = (k - 1 >= 2);
+            if (more) {
+              st.load(k - 3, reinterpret_cast<float*>(z));
+              const float s2 = sSl[k - 3];
+#pragma unroll
+              for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+            }
+            cta_sync();
+            gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
+#pragma unroll
+            for (int jj = 0; jj < kJT; ++jj) {
+              bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
+              if (more) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
+            }
+            cta_sync();
+          }
+          // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
+          for (int t4 = tid; t4 < 4 * N; t4 += T) {
+            const int qq = t4 & 3, j = t4 >> 2;
+            float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
 #pragma unroll 4
-          for (int p = qq; p < C::P; p += 4) {
-            const float4 zb = bufZ[j * C::PSTR + p];
-            a0 = fmaf(zb.x, sX[p], a0) + zb.y;
-            a1 = fmaf(zb.x, sY[p], a1) + zb.z;
-            ab += zb.x;
-          }
-          const unsigned mk = __activemask();
+            for (int p = qq; p < C::P; p += 4) {
+              const float4 zb = bufZ[j * C::PSTR + p];
+              a0 = fmaf(zb.x, sX[p], a0) + zb.y;
+              a1 = fmaf(zb.x, sY[p], a1) + zb.z;
+              ab += zb.x;
+            }
+            const unsigned mk = __activemask();
 #pragma unroll
-          for (int o = 1; o < 4; o <<= 1) {
-            a0 += __shfl_xor_sync(mk, a0, o);
-            a1 += __shfl_xor_sync(mk, a1, o);
-            ab += __shfl_xor_sync(mk, ab, o);
+            for (int o = 1; o < 4; o <<= 1) {
+              a0 += __shfl_xor_sync(mk, a0, o);
+              a1 += __shfl_xor_sync(mk, a1, o);
+              ab += __shfl_xor_sync(mk, ab, o);
+            }
+            if (qq == 0) {
+              acc_add<DSM>(A, LY::offW(1) + 2 * j, a0, first);
+              acc_add<DSM>(A, LY::offW(1) + 2 * j + 1, a1, first);
+              acc_add<DSM>(A, LY::offB(1) + j, ab, first);
+            }
           }
-          if (qq == 0) {
-            acc_add<DSM>(A, LY::offW(1) + 2 * j, a0, first);
-            acc_add<DSM>(A, LY::offW(1) + 2 * j + 1, a1, first);
-            acc_add<DSM>(A, LY::offB(1) + j, ab, first);
+          // the slope entries of the partial stay 0 (K5 fills them)
+          if (tid == 0 && first && !DSM) {
+#pragma unroll
+            for (int k = 1; k <= NH; ++k) Pc[LY::offA(k)] = 0.0f;
           }
-        }
-        // the slope entries of the partial stay 0 (K5 fills them)
-        if (tid == 0 && first && !DSM) {
-#pragma unroll
-          for (int k = 1; k <= NH; ++k) Pc[LY::offA(k)] = 0.0f;
-        }
-      }
-    }
-    if constexpr (MODE == 0) {
-      // loss partials of the chunk: fixed-order block reduction once per chunk
-      if (ntiles > 0) {
-        block_sum<4, T>(lsum, sRed);
-        if (tid == 0) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r) a.partial_loss[size_t(c) * 4 + r] = lsum[r];
         }
       }
+      if constexpr (MODE == 0) {
+        // loss partials of the chunk: fixed-order block reduction once per chunk
+        if (ntiles > 0) {
+          block_sum<4, T>(lsum, sRed);
+          if (tid == 0) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a.partial_loss[size_t(c) * 4 + r] = lsum[r];
+          }
+        }
+      }
+    };
+    if constexpr (ACT == kActMixed) {
+      if (act == 0)
+        chunk_body(std::integral_constant<int, 0>{});
+      else if (act == 1)
+        chunk_body(std::integral_constant<int, 1>{});
+      else
+        chunk_body(std::integral_constant<int, 2>{});
+    } else {
+      chunk_body(std::integral_constant<int, ACT>{});
     }
     if constexpr (MODE == 0 && DSM) {
       // flush the chunk's gradient (slope slots stay 0; K5 fills them)
