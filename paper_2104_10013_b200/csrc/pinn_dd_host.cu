@@ -168,6 +168,7 @@ struct pinn_dd {
   float *partial = nullptr, *partial_loss = nullptr, *payload = nullptr, *loss = nullptr;
   float *pinv = nullptr, *gstash = nullptr, *scratch = nullptr;
   int32_t *pinfo = nullptr, *ptwin = nullptr, *sub_chunk = nullptr, *tstep = nullptr, *done = nullptr;
+  double* slope_part = nullptr;
   int32_t *flag = nullptr, *packmap = nullptr, *sub_act = nullptr, *order1 = nullptr, *sched = nullptr;
   float2* segn = nullptr;
   float4 *sub_w = nullptr, *sub_adam = nullptr;
@@ -252,7 +253,7 @@ struct Carve {
 struct Layout {
   size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ord1,
       sched, ch2, subch,
-      tstep, done, flag, loss, packmap, gstash, total;
+      tstep, done, flag, loss, packmap, slopep, gstash, total;
 };
 
 // validation + planning shared by workspace_size and create
@@ -379,6 +380,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->flag = c.take<int32_t>(1);
   L->loss = c.take<float>(ns * 8);
   L->packmap = c.take<int32_t>(size_t(pstride));
+  L->slopep = c.take<double>(ns * size_t((pstride + kRB - 1) / kRB) * kMaxHidden);
   L->gstash = (d->flags & PINN_DD_FLAG_GLOBAL_STASH)
                   ? c.take<float>(size_t(grid1) * d->n_hidden * kA * ops->threads)
                   : c.off;
@@ -453,6 +455,7 @@ RArgs make_rargs(pinn_dd* h, int mode) {
   r.sub_adam = h->sub_adam;
   r.loss = h->loss;
   r.flag = h->flag;
+  r.slope_part = h->slope_part;
   r.mode = mode;
   h->ops->slopetab(r);
   return r;
@@ -626,6 +629,7 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->tstep = reinterpret_cast<int32_t*>(base + L.tstep);
   h->done = reinterpret_cast<int32_t*>(base + L.done);
   h->flag = reinterpret_cast<int32_t*>(base + L.flag);
+  h->slope_part = reinterpret_cast<double*>(base + L.slopep);
   h->loss = reinterpret_cast<float*>(base + L.loss);
   h->packmap = reinterpret_cast<int32_t*>(base + L.packmap);
   h->gstash = reinterpret_cast<float*>(base + L.gstash);

@@ -776,61 +776,103 @@ struct RArgs {
   const float4* sub_adam;     // lr, beta1, beta2, eps
   float* loss;                // [n_sub][8]
   int32_t* flag;              // non-finite flag
+  double* slope_part;         // [n_sub][gridDim.x][kMaxHidden] per-block slope partials (K5a -> K5b)
   int mode;                   // k_slope_adam: 0 slopes only, 1 slopes + Adam
   int n_hidden;               // 0: skip the slope pass
   int offW[kMaxHidden], nW[kMaxHidden], offB[kMaxHidden], nB[kMaxHidden], offA[kMaxHidden];
 };
 
 __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
+  __shared__ double red[kRB / 32];
   const int q = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.x * kRB;
+  const int i = i0 + tid;
   const int c0 = r.sub_chunk[q], c1 = r.sub_chunk[q + 1];
+  const float* P = r.params + size_t(q) * r.pstride;
+  float g = 0.0f;
   if (i < r.pstride) {
-    float g = 0.0f;
-    for (int c = c0; c < c1; ++c) g += r.partial[size_t(c) * r.pstride + i];
+    // chunk order, 8 loads in flight per thread
+    int c = c0;
+    for (; c + 8 <= c1; c += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(r.partial + size_t(c + u) * r.pstride + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) g += v[u];
+    }
+    for (; c < c1; ++c) g += __ldcg(r.partial + size_t(c) * r.pstride + i);
     r.grad[size_t(q) * r.pstride + i] = g;
     if (!isfinite(g)) atomicOr(r.flag, 2);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    float l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    for (int c = c0; c < c1; ++c)
-      for (int e = 0; e < 4; ++e) l[e] += r.partial_loss[size_t(c) * 4 + e];
-    const float4 w = r.sub_w[q];
-    const float J = w.x * l[0] + w.y * l[1] + w.z * l[2] + w.w * l[3];
-    float* L = r.loss + size_t(q) * 8;
-    L[0] = l[0]; L[1] = l[1]; L[2] = l[2]; L[3] = l[3]; L[4] = J;
-    L[5] = isfinite(J) ? 0.0f : 1.0f;
-    L[6] = 0.0f; L[7] = 0.0f;
-    if (!isfinite(J)) atomicOr(r.flag, 1);
-  }
-}
-
-__global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
-  __shared__ double red[kRB / 32];
-  const int q = blockIdx.y;
-  const int i0 = blockIdx.x * kRB;
-  const int tid = threadIdx.x;
-  const float* P = r.params + size_t(q) * r.pstride;
-  float* G = r.grad + size_t(q) * r.pstride;
+  // per-block partial sums of <W^k, dJ/dW^k> + <b^k, dJ/db^k> (fp64, fixed
+  // order) for the slope identity; K5b combines them (no cross-block reads of
+  // parameters that K5b's Adam updates)
   for (int k = 0; k < r.n_hidden; ++k) {
-    const int oa = r.offA[k];
-    if (oa < i0 || oa >= i0 + kRB) continue;   // block-uniform
-    double acc = 0.0;
-    for (int e = tid; e < r.nW[k]; e += kRB) acc += double(P[r.offW[k] + e]) * double(G[r.offW[k] + e]);
-    for (int e = tid; e < r.nB[k]; e += kRB) acc += double(P[r.offB[k] + e]) * double(G[r.offB[k] + e]);
+    const int w0 = r.offW[k], w1 = w0 + r.nW[k], b0 = r.offB[k], b1 = b0 + r.nB[k];
+    double* slot = r.slope_part + (size_t(q) * gridDim.x + blockIdx.x) * kMaxHidden + k;
+    const bool hit = (w0 < i0 + kRB && w1 > i0) || (b0 < i0 + kRB && b1 > i0);   // block-uniform
+    if (!hit) {
+      if (tid == 0) *slot = 0.0;
+      continue;
+    }
+    double acc = ((i >= w0 && i < w1) || (i >= b0 && i < b1)) ? double(P[i]) * double(g) : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((tid & 31) == 0) red[tid >> 5] = acc;
     __syncthreads();
     if (tid == 0) {
-      double s = 0.0;
-      for (int w = 0; w < kRB / 32; ++w) s += red[w];
-      const float ga = float(s / double(P[oa]));
-      G[oa] = ga;
-      if (!isfinite(ga)) atomicOr(r.flag, 4);
+      double sum = 0.0;
+      for (int w = 0; w < kRB / 32; ++w) sum += red[w];
+      *slot = sum;
     }
     __syncthreads();
   }
+  if (blockIdx.x == 0 && tid < 32) {
+    // loss terms of subdomain q: lane l sums chunks c0 + l, c0 + l + 32, ...; fixed shuffle tree
+    float4 l4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    for (int c = c0 + tid; c < c1; c += 32) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(r.partial_loss) + c);
+      l4.x += v.x; l4.y += v.y; l4.z += v.z; l4.w += v.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l4.x += __shfl_xor_sync(0xffffffffu, l4.x, o);
+      l4.y += __shfl_xor_sync(0xffffffffu, l4.y, o);
+      l4.z += __shfl_xor_sync(0xffffffffu, l4.z, o);
+      l4.w += __shfl_xor_sync(0xffffffffu, l4.w, o);
+    }
+    if (tid == 0) {
+      const float4 w = r.sub_w[q];
+      const float J = w.x * l4.x + w.y * l4.y + w.z * l4.z + w.w * l4.w;
+      float* L = r.loss + size_t(q) * 8;
+      L[0] = l4.x; L[1] = l4.y; L[2] = l4.z; L[3] = l4.w; L[4] = J;
+      L[5] = isfinite(J) ? 0.0f : 1.0f;
+      L[6] = 0.0f; L[7] = 0.0f;
+      if (!isfinite(J)) atomicOr(r.flag, 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
+  const int q = blockIdx.y;
+  const int i0 = blockIdx.x * kRB;
+  const int tid = threadIdx.x;
+  const float* P = r.params + size_t(q) * r.pstride;
+  float* G = r.grad + size_t(q) * r.pstride;
+  // slope gradients: the block owning a^k combines K5a's
+  // per-block partials in block order
+  if (tid < r.n_hidden) {
+    const int oa = r.offA[tid];
+    if (oa >= i0 && oa < i0 + kRB) {
+      double sum = 0.0;
+      for (int b = 0; b < int(gridDim.x); ++b) sum += r.slope_part[(size_t(q) * gridDim.x + b) * kMaxHidden + tid];
+      const float ga = float(sum / double(P[oa]));
+      G[oa] = ga;
+      if (!isfinite(ga)) atomicOr(r.flag, 4);
+    }
+  }
+  __syncthreads();
   if (r.mode == 0) return;
   const int i = i0 + tid;
   const int t = r.tstep[q] + 1;
@@ -859,7 +901,6 @@ __global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
   }
 }
 
-// packed <-> internal parameter layout
 __global__ void k_gather(const float* src, const int32_t* map, int n, int pstride, int sub_stride_dst,
                          float* dst, int n_sub) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

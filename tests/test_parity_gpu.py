@@ -277,6 +277,23 @@ def test_train_steps_track_oracle():
     m.close()
 
 
+def test_training_steps_bitwise_reproducible():
+    """20 graph-replayed loss+grad+Adam steps, twice from the same seeded
+    start: parameters, Adam moments and losses are bitwise equal (K5a writes
+    per-block slope partials, so K5b's Adam never races the slope reduction)."""
+    prob = make_config("C2", method="xpinn", n_f=400, n_i=25, n_u=20)
+    runs = []
+    for _ in range(2):
+        m = _handle(prob)
+        out = m.step(20)
+        torch.cuda.synchronize()
+        runs.append((np.array(out), [torch.cat([m.get(q, w) for w in (0, 1, 2)]).cpu() for q in range(prob.n_sub)]))
+        m.close()
+    assert np.array_equal(runs[0][0], runs[1][0])
+    for a, b in zip(runs[0][1], runs[1][1]):
+        assert torch.equal(a, b)
+
+
 def test_placement_invariance_two_handles():
     """Same decomposition as one handle or split over two 'ranks' (payload rows
     moved by the exchange plan): losses and gradients are bitwise equal."""
