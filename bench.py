@@ -354,6 +354,9 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (K1, fused loss + grad)
     k1_flops, k2_flops = algorithmic_flops(h_prob, local)
+    fused = world == 1 and args.method != "dp" and h.step_fused
+    if fused:
+        k1_flops += k2_flops          # the fused step runs K2's payload chunks inside K1
     k1_ms = kt[1] / args.steps
     k1_what = "K1 per launch (CUDA events inside the timed region)"
     if world > 1:
@@ -395,7 +398,8 @@ def run_ours(args):
                                             **({"gpus": 8} if args.workload == "c3" else {})))
         acts = sorted({prob.act(q) for q in local})
         kname = (f"K1 k_fused<{prob.width},{prob.n_hidden},{prob.d_out},"
-                 f"{'mixed' if len(acts) > 1 else acts[0]}> (fused fwd jets + loss + reverse)")
+                 f"{'mixed' if len(acts) > 1 else acts[0]}> (fused fwd jets + loss + reverse"
+                 f"{'; K2 interface payload in the same launch' if fused else ''})")
         share = kt[1] / max(1e-9, sum(kt[:3])) if world == 1 else k1_ms / (t_max / args.steps)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -415,7 +419,8 @@ def run_ours(args):
                          "k1_ms_per_launch": k1_ms, "k1_timing": k1_what, "k1_gflop_per_launch": k1_flops / 1e9,
                          "k1_share_of_step": share,
                          "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md clocks.max.sm)"},
-            "kernels_ms_per_step": {"K2_payload": kt[0] / args.steps if world == 1 else None,
+            "kernels_ms_per_step": {"K2_payload": (0.0 if fused else kt[0] / args.steps) if world == 1 else None,
+                                    "K2_inside_K1": fused,
                                     "K1_loss_grad": k1_ms,
                                     "K5_reduce_adam": kt[2] / args.steps if world == 1 else None},
             "gpu_launches": int(kt[3]),

@@ -212,8 +212,16 @@ pinn_dd_status pinn_dd_get_step(pinn_dd* h, int32_t sub, int32_t* t);
 
 /* With PINN_DD_FLAG_TIMING: cumulative device milliseconds of
    {K2 payload, K1 loss+grad, K5 reduce/adam, launches counted} since the last
-   call (synchronises, then resets). */
+   call (synchronises, then resets).  When pinn_dd_step runs fused (below) K2's
+   work is inside K1 and its entry is 0. */
 pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4);
+
+/* 1 if pinn_dd_step runs the interface payload (K2) and the loss + gradient
+   (K1) as one persistent launch: payload chunks first, interface loss chunks
+   wait on a device counter of finished payload chunks (Algorithm 1 lines
+   238-262, with every neighbour on this GPU: n_recv == 0).
+   0 otherwise (point-per-thread kernel, remote twins, or no interface). */
+int32_t pinn_dd_step_fused(const pinn_dd* h);
 
 /* Tile geometry chosen for this handle: {points per tile P, tiles per chunk,
    number of chunks, grid size}. */

@@ -32,7 +32,7 @@ EXPORTS = [
     "pinn_dd_payload_buffer", "pinn_dd_loss_grad", "pinn_dd_loss_grad_interior", "pinn_dd_loss_grad_interface",
     "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict",
     "pinn_dd_get_params", "pinn_dd_set_params", "pinn_dd_get_step", "pinn_dd_kernel_times",
-    "pinn_dd_plan_info", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
+    "pinn_dd_plan_info", "pinn_dd_step_fused", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
 ]
 
 
@@ -96,13 +96,15 @@ def load_library(path: str = LIB_PATH):
     lib.pinn_dd_get_step.argtypes = [vp, i32, C.POINTER(i32)]
     lib.pinn_dd_kernel_times.argtypes = [vp, C.POINTER(C.c_double)]
     lib.pinn_dd_plan_info.argtypes = [vp, C.POINTER(i64)]
+    lib.pinn_dd_step_fused.argtypes = [vp]
+    lib.pinn_dd_step_fused.restype = i32
     lib.pinn_dd_debug_buffer.argtypes = [vp, i32, C.POINTER(vp), C.POINTER(i64)]
     lib.pinn_dd_destroy.argtypes = [vp]
     lib.pinn_dd_destroy.restype = None
     lib.pinn_dd_last_error.argtypes = [vp]
     lib.pinn_dd_last_error.restype = C.c_char_p
     for name in EXPORTS:
-        if name not in ("pinn_dd_n_params", "pinn_dd_destroy", "pinn_dd_last_error"):
+        if name not in ("pinn_dd_n_params", "pinn_dd_destroy", "pinn_dd_last_error", "pinn_dd_step_fused"):
             getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -386,6 +388,11 @@ class PinnDD:
         t = C.c_int32()
         self._check(self.lib.pinn_dd_get_step(self.h, q, C.byref(t)))
         return t.value
+
+    @property
+    def step_fused(self) -> bool:
+        """pinn_dd_step runs K2 (payload) inside K1's persistent launch."""
+        return bool(self.lib.pinn_dd_step_fused(self.h))
 
     def kernel_times(self):
         ms = (C.c_double * 4)()

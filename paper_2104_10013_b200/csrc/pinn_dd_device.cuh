@@ -437,6 +437,12 @@ struct Chunk {
   int32_t pad;
 };
 
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 struct KArgs {
   const float* coords;      // [2][n_points]
   const float* target;      // [DO][n_points]
@@ -449,8 +455,10 @@ struct KArgs {
   const int32_t* sub_act;   // [n_sub] activation per subdomain (read only by kActMixed instances)
   const float4* sub_w;      // [n_sub] (w_u, w_f, w_i, w_if)
   const Chunk* chunks;
+  const Chunk* chunks2;     // payload chunks (MODE 2: the fused step runs them first)
+  int n_chunks2;
   const int32_t* order;     // [n_chunks] processing order (nullptr = identity)
-  int32_t* sched;           // [2] chunk counter, CTAs done (zero between launches)
+  int32_t* sched;           // chunk counter, CTAs done (zero between launches); MODE 2: [4] payload chunks done
   int n_chunks;
   int64_t n_points;
   int pstride;              // floats per subdomain in params / partial

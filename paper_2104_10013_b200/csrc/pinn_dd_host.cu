@@ -40,6 +40,7 @@ struct Ops {
   size_t smem;     // dynamic smem of the fused kernel
   void (*k1)(const KArgs&, int grid, size_t smem, cudaStream_t);
   void (*k2)(const KArgs&, int grid, size_t smem, cudaStream_t);
+  void (*kf)(const KArgs&, int grid, size_t smem, cudaStream_t);   // fused payload + loss/grad (nullptr: none)
   void (*pred)(const float*, int, float, const float*, const int32_t*, int64_t, float*, const int32_t*,
                cudaStream_t);
   void (*packmap)(std::vector<int32_t>&);
@@ -70,6 +71,9 @@ struct Inst {
       k_fused_pt<N, NH, DO, ACT, 1><<<grid, kPT, sm, s>>>(a);
     else
       k_fused<N, NH, DO, ACT, 1, T><<<grid, T, sm, s>>>(a);
+  }
+  static void kf(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
+    if constexpr (!PT) k_fused<N, NH, DO, ACT, 2, T><<<grid, T, sm, s>>>(a);
   }
   static void pred(const float* params, int pstride, float sn, const float* pts, const int32_t* own, int64_t n,
                    float* out, const int32_t* sub_act, cudaStream_t s) {
@@ -110,6 +114,8 @@ struct Inst {
       e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, attr, int(sm));
       if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, carve, 100);
       if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, carve, 100);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 2, T>, carve, 100);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 2, T>, attr, int(sm));
       if (e != cudaSuccess) return e;
       return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, attr, int(sm));
     }
@@ -118,7 +124,7 @@ struct Inst {
     static_assert(NH <= kMaxHidden, "too many hidden layers");
     if constexpr (PT) static_assert(PtCfg<N, NH, DO>::P == C::P, "both kernels tile by the same point count");
     return Ops{N, NH, DO, ACT, PT ? 1 : 0, LY::total(), C::P, PT ? kPT : T, PT ? 1 : C::CPS, smem(), &k1, &k2,
-               &pred, &packmap, &slopetab, &setattr};
+               PT ? nullptr : &kf, &pred, &packmap, &slopetab, &setattr};
   }
 };
 
@@ -372,7 +378,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->suba = c.take<float4>(ns);
   L->ch1 = c.take<Chunk>(size_t(n1));
   L->ord1 = c.take<int32_t>(size_t(2 * n1));   // [all | interior, interface] processing orders
-  L->sched = c.take<int32_t>(4);
+  L->sched = c.take<int32_t>(8);   // [0,1] K1, [2,3] K2, [4] fused step: payload chunks done
   L->ch2 = c.take<Chunk>(size_t(n2) + 1);
   L->subch = c.take<int32_t>(ns + 1);
   L->tstep = c.take<int32_t>(ns);
@@ -419,6 +425,8 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.sub_w = h->sub_w;
   a.sub_act = h->sub_act;
   a.chunks = payload_tiles ? h->chunks2 : h->chunks1;
+  a.chunks2 = nullptr;
+  a.n_chunks2 = 0;
   a.order = payload_tiles ? nullptr : h->order1;   // launch_k1 selects the part
   a.sched = h->sched + (payload_tiles ? 2 : 0);
   a.n_chunks = payload_tiles ? h->n_chunks2 : h->n_chunks1;
@@ -512,10 +520,10 @@ pinn_dd_status record(pinn_dd* h, int i, bool capturing) {
   return PINN_DD_OK;
 }
 
-pinn_dd_status accumulate_times(pinn_dd* h) {
+pinn_dd_status accumulate_times(pinn_dd* h, bool fused = false) {
   CK(h, cudaEventSynchronize(h->ev[3]));
   float a = 0, b = 0, c = 0;
-  CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+  if (!fused) CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
   CK(h, cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
   CK(h, cudaEventElapsedTime(&c, h->ev[2], h->ev[3]));
   h->ms[0] += a;
@@ -524,9 +532,37 @@ pinn_dd_status accumulate_times(pinn_dd* h) {
   return PINN_DD_OK;
 }
 
+// K2 and K1 as one persistent launch (payload chunks first, interface loss
+// chunks wait on the payload-done counter); all twins must be local
+pinn_dd_status launch_fused(pinn_dd* h) {
+  KArgs a = make_kargs(h, false);
+  a.chunks2 = h->chunks2;
+  a.n_chunks2 = h->n_chunks2;
+  h->ops->kf(a, std::min(h->grid1, a.n_chunks + a.n_chunks2), h->ops->smem, h->stream);
+  ++h->launches;
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+
+bool use_fused(const pinn_dd* h) {
+  static const bool off = std::getenv("PINN_DD_NO_FUSED_STEP") != nullptr;   // development A/B knob
+  return h->ops->kf && h->n_chunks2 > 0 && h->d.n_recv == 0 && !off;
+}
+
 pinn_dd_status one_iteration(pinn_dd* h, bool timed, bool capturing) {
   pinn_dd_status s;
-  if (timed && (s = record(h, 0, capturing)) != PINN_DD_OK) return s;
+  if (timed && !use_fused(h) && (s = record(h, 0, capturing)) != PINN_DD_OK) return s;
+  if (use_fused(h)) {
+    // K2 folded into K1 (reported as 0 ms); three event nodes, not four: each
+    // event-record node costs ~2.7 us of step latency on the B200
+    if (timed && (s = record(h, 1, capturing)) != PINN_DD_OK) return s;
+    if ((s = launch_fused(h)) != PINN_DD_OK) return s;
+    if (timed && (s = record(h, 2, capturing)) != PINN_DD_OK) return s;
+    if ((s = launch_k5(h, 1)) != PINN_DD_OK) return s;
+    if (timed && (s = record(h, 3, capturing)) != PINN_DD_OK) return s;
+    if (timed && !capturing) return accumulate_times(h, true);
+    return PINN_DD_OK;
+  }
   if ((s = launch_k2(h)) != PINN_DD_OK) return s;
   if (timed && (s = record(h, 1, capturing)) != PINN_DD_OK) return s;
   if ((s = launch_k1(h)) != PINN_DD_OK) return s;
@@ -751,7 +787,7 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   CKC(cudaMemcpyAsync(h->sub_adam, suba.data(), suba.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->chunks1, c1.data(), c1.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->order1, ord1.data(), ord1.size() * 4, cudaMemcpyHostToDevice, st));
-  CKC(cudaMemsetAsync(h->sched, 0, 4 * sizeof(int32_t), st));
+  CKC(cudaMemsetAsync(h->sched, 0, 8 * sizeof(int32_t), st));
   if (!c2.empty())
     CKC(cudaMemcpyAsync(h->chunks2, c2.data(), c2.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->sub_chunk, subch.data(), subch.size() * 4, cudaMemcpyHostToDevice, st));
@@ -885,8 +921,8 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
       CK(h, cudaGraphLaunch(h->gexec, h->gstream));
       CK(h, cudaEventRecord(h->gjoin[1], h->gstream));
       CK(h, cudaStreamWaitEvent(h->stream, h->gjoin[1], 0));
-      h->launches += (h->n_chunks2 > 0 ? 4 : 3);
-      if (timed && (s = accumulate_times(h)) != PINN_DD_OK) return s;
+      h->launches += use_fused(h) ? 3 : (h->n_chunks2 > 0 ? 4 : 3);
+      if (timed && (s = accumulate_times(h, use_fused(h))) != PINN_DD_OK) return s;
     } else if ((s = one_iteration(h, timed, false)) != PINN_DD_OK) {
       return s;
     }
@@ -966,6 +1002,8 @@ pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4) {
   h->launches = 0;
   return PINN_DD_OK;
 }
+
+int32_t pinn_dd_step_fused(const pinn_dd* h) { return h && use_fused(h) ? 1 : 0; }
 
 pinn_dd_status pinn_dd_plan_info(pinn_dd* h, int64_t* info4) {
   if (!h || !info4) return fail(h, PINN_DD_EINVAL, "bad plan_info arguments");

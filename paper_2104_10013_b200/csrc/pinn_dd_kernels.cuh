@@ -375,10 +375,10 @@ __device__ __forceinline__ void point_adjoint(const KArgs& a, int64_t gp, float 
     }
   } else {
     // interface point: neighbour payload is a constant
-    const float* q = a.payload + size_t(a.ptwin[gp]) * NF;
+    const float* q = a.payload + size_t(a.ptwin[gp]) * NF;   // read via L2 (__ldcg): rows written by other CTAs
 #pragma unroll
     for (int o = 0; o < DO; ++o) {
-      const float d = U[o].x - q[o];   // u_q - {{u}} = d / 2  (Z1)
+      const float d = U[o].x - __ldcg(q + o);   // u_q - {{u}} = d / 2  (Z1)
       lsum[2] += inv * 0.25f * d * d;
       Ub[o].x += 0.5f * lw.z * inv * d;
     }
@@ -390,7 +390,7 @@ __device__ __forceinline__ void point_adjoint(const KArgs& a, int64_t gp, float 
       ne = pde_residual<DO>(a.pc, U, x, y, r, dr);
     }
     for (int e = 0; e < ne; ++e) {
-      const float d = r[e] - q[DO + e];
+      const float d = r[e] - __ldcg(q + DO + e);
       lsum[3] += inv * d * d;
       const float cf = 2.0f * lw.w * inv * d;
 #pragma unroll
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   st.nthr = T;
   st.g = nullptr;
   st.taddr = 0;
-  if constexpr (MODE == 0) {
+  if constexpr (MODE != 1) {
     if (a.gstash == nullptr) {
       if (tid < 32) {
         __syncwarp();
@@ -456,16 +456,30 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   // chunks first, one-tile chunks last), so the tail is one tile long.  Which
   // CTA runs a chunk never changes its result: every chunk owns its partial
   // slot and K5 sums the slots in a fixed order.
+  // MODE 2 (the fused single-GPU step): indices [0, n_chunks2) are the
+  // payload chunks (K2's work), then the loss chunks; an interface loss chunk
+  // waits until every payload chunk is done (all CTAs are resident and payload
+  // chunks are handed out first, so the wait always ends).
   __shared__ int s_next;
   int cur_sub = -1;
+  const int n_pay = MODE == 2 ? a.n_chunks2 : 0;
 #pragma unroll 1
   for (;;) {
     if (tid == 0) s_next = atomicAdd(a.sched, 1);
     cta_sync();
     const int idx = s_next;
-    if (idx >= a.n_chunks) break;
-    const int c = a.order ? a.order[idx] : idx;
-    const Chunk ch = a.chunks[c];
+    if (idx >= a.n_chunks + n_pay) break;
+    const bool pay = MODE == 1 || (MODE == 2 && idx < n_pay);   // payload chunk (forward + payload epilogue)
+    const int li = idx - n_pay;
+    const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (a.order ? a.order[li] : li);
+    const Chunk ch = (MODE == 2 && pay) ? a.chunks2[c] : a.chunks[c];
+    if (MODE == 2 && !pay && ch.pad) {
+      // interface loss chunk: acquire the completed payload rows
+      if (tid == 0) {
+        while (ld_acquire_gpu(a.sched + 4) < n_pay) __nanosleep(64);
+      }
+      cta_sync();
+    }
     if (ch.sub != cur_sub) {
       cta_sync();
       load_weights<N, NH, DO, T>(a.params + size_t(ch.sub) * a.pstride, a.slope_n, sm);
@@ -475,12 +489,12 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     const int act = ACT == kActMixed ? a.sub_act[ch.sub] : ACT;   // uniform per chunk
     float* Pc = a.partial + size_t(c) * a.pstride;
     float* A = DSM ? sAcc : Pc;   // gradient accumulator of this chunk
-    if constexpr (MODE == 0 && DSM) {
+    if (DSM && !pay) {
       cta_sync();
       for (int e = tid; e < C::ACC; e += T) sAcc[e] = 0.0f;
     }
     const int ntiles = (ch.count + C::P - 1) / C::P;
-    if constexpr (MODE == 0) {
+    if (!pay) {
       if (ntiles == 0) {   // a subdomain without points: its slot holds zeros
         if (!DSM)
           for (int e = tid; e < a.pstride; e += T) Pc[e] = 0.0f;
@@ -490,8 +504,9 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     // the chunk's tiles, compiled once per activation: the per-subdomain-activation
     // instance dispatches here per chunk, so each hot loop holds one activation
     // path only (three inlined paths overflowed the instruction cache)
-    auto chunk_body = [&](auto act_c) {
+    auto chunk_body = [&](auto act_c, auto mode_c) {
       constexpr int AS = decltype(act_c)::value;
+      constexpr int MS = decltype(mode_c)::value;   // 0 loss + gradient, 1 payload
       // coordinates of the next tile are loaded into registers while the
       // current tile computes (thread p < P owns point p of a tile)
       static_assert(C::P <= T, "one staged point per thread");
@@ -532,7 +547,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           const float s = sSl[0];
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
-          if constexpr (MODE == 0) st.store(0, reinterpret_cast<const float*>(z));
+          if constexpr (MS == 0) st.store(0, reinterpret_cast<const float*>(z));
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
         }
@@ -545,7 +560,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           const float s = sSl[k - 1];
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
-          if constexpr (MODE == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
+          if constexpr (MS == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
           cta_sync();
@@ -569,7 +584,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         cta_sync();
 
         // ----------------------------------------------------------- epilogue
-        if constexpr (MODE == 1) {
+        if constexpr (MS == 1) {
           // payload: u(x_I) and f.n (cPINN) or F (XPINN) (Algorithm 1)
           for (int p = tid; p < np; p += T) {
             float4 U[DO];
@@ -702,7 +717,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           }
         }
       }
-      if constexpr (MODE == 0) {
+      if constexpr (MS == 0) {
         // loss partials of the chunk: fixed-order block reduction once per chunk
         if (ntiles > 0) {
           block_sum<4, T>(lsum, sRed);
@@ -713,17 +728,35 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         }
       }
     };
+    auto by_mode = [&](auto act_c) {
+      if constexpr (MODE == 2) {
+        if (pay)
+          chunk_body(act_c, std::integral_constant<int, 1>{});
+        else
+          chunk_body(act_c, std::integral_constant<int, 0>{});
+      } else {
+        chunk_body(act_c, std::integral_constant<int, MODE>{});
+      }
+    };
     if constexpr (ACT == kActMixed) {
       if (act == 0)
-        chunk_body(std::integral_constant<int, 0>{});
+        by_mode(std::integral_constant<int, 0>{});
       else if (act == 1)
-        chunk_body(std::integral_constant<int, 1>{});
+        by_mode(std::integral_constant<int, 1>{});
       else
-        chunk_body(std::integral_constant<int, 2>{});
+        by_mode(std::integral_constant<int, 2>{});
     } else {
-      chunk_body(std::integral_constant<int, ACT>{});
+      by_mode(std::integral_constant<int, ACT>{});
     }
-    if constexpr (MODE == 0 && DSM) {
+    if (MODE == 2 && pay) {
+      // publish this payload chunk (release: all its rows are written)
+      cta_sync();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(a.sched + 4, 1);
+      }
+    }
+    if (DSM && !pay) {
       // flush the chunk's gradient (slope slots stay 0; K5 fills them)
       cta_sync();
       for (int e = tid; e < C::ACC; e += T) Pc[e] = sAcc[e];
@@ -736,10 +769,11 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     if (atomicAdd(a.sched + 1, 1) == int(gridDim.x) - 1) {
       a.sched[0] = 0;
       a.sched[1] = 0;
+      if (MODE == 2) a.sched[4] = 0;
       __threadfence();
     }
   }
-  if constexpr (MODE == 0) {
+  if constexpr (MODE != 1) {
     if (a.gstash == nullptr) {
       cta_sync();
       tmem_fence_after();

@@ -294,6 +294,30 @@ def test_training_steps_bitwise_reproducible():
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("cfg,kw", [("C2", dict(method="cpinn", n_f=400, n_i=25, n_u=20)),
+                                    ("C3", dict(gpus=2, n_f=600, n_i=30, n_u=40))])
+def test_fused_step_equals_phased_calls(cfg, kw):
+    """pinn_dd_step with K2 folded into K1's persistent launch (payload chunks
+    first, interface loss chunks behind a device counter) gives bitwise the
+    same losses, gradient and updated parameters as the separate calls
+    interface_payload -> loss_grad -> adam."""
+    prob = make_config(cfg, **kw)
+    a = _handle(prob)
+    assert a.step_fused
+    out = a.step(1)
+    b = _handle(prob)
+    b.interface_payload()
+    lb, gb = b.loss_grad()
+    b.adam()
+    torch.cuda.synchronize()
+    for q in range(prob.n_sub):
+        assert np.array_equal(np.asarray(out[q, :5]), lb[q, :5].cpu().numpy()), q
+        assert torch.equal(a.get(q, 3), b.get(q, 3)), q
+        assert torch.equal(a.get(q, 0), b.get(q, 0)), q
+    a.close()
+    b.close()
+
+
 def test_placement_invariance_two_handles():
     """Same decomposition as one handle or split over two 'ranks' (payload rows
     moved by the exchange plan): losses and gradients are bitwise equal."""
