@@ -422,7 +422,10 @@ def exchange_payload(payload: torch.Tensor, plan: ExchangePlan, group=None, wait
     import torch.distributed as dist
     if not plan.send and not plan.recv:
         return []
-    ops, bufs = [], []
+    # gloo moves host memory only: CUDA payload rows are staged through the host
+    # (test / CPU-cluster path; NCCL sends the device rows directly)
+    stage = payload.is_cuda and dist.get_backend(group) == "gloo"
+    ops, bufs, landing = [], [], []
     cache = plan.__dict__.setdefault("_idx_cache", {})
     for peer in sorted(set(plan.send) | set(plan.recv)):
         if peer in plan.send:
@@ -431,15 +434,24 @@ def exchange_payload(payload: torch.Tensor, plan: ExchangePlan, group=None, wait
                 cache[key] = torch.as_tensor(plan.send[peer], device=payload.device)
             idx = cache[key]
             sbuf = payload.index_select(0, idx).contiguous()
+            if stage:
+                sbuf = sbuf.cpu()
             bufs.append(sbuf)
             ops.append(dist.P2POp(dist.isend, sbuf, peer, group))
         if peer in plan.recv:
             r0, n = plan.recv[peer]
-            ops.append(dist.P2POp(dist.irecv, payload[r0:r0 + n], peer, group))
+            if stage:
+                rbuf = torch.empty(n, payload.shape[1], dtype=payload.dtype)
+                landing.append((r0, n, rbuf))
+            else:
+                rbuf = payload[r0:r0 + n]
+            ops.append(dist.P2POp(dist.irecv, rbuf, peer, group))
     reqs = dist.batch_isend_irecv(ops)
-    if wait:
+    if wait or stage:
         for req in reqs:
             req.wait()
+        for r0, n, rbuf in landing:
+            payload[r0:r0 + n].copy_(rbuf)
         return []
     return reqs
 
