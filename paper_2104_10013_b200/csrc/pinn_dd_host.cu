@@ -216,9 +216,19 @@ pinn_dd_status fail(pinn_dd* h, pinn_dd_status s, const char* fmt, ...) {
 int n_eq_of(int pde) { return pde == PINN_DD_PDE_NS ? 3 : 1; }
 
 // tiles per chunk of a subdomain with `cnt` points: >= 4 tiles, <= ~128 chunks
+// Tiles per full chunk of a run of `cnt` points: at most ~128 chunks per run;
+// runs of >= 200 tiles use >= 4-tile chunks (fewer partial slots to flush and
+// reduce), shorter runs (the small C5 regions) 1-tile chunks so the persistent
+// schedule's tail stays one tile long (C5 K1 0.573 -> 0.531 ms).  Depends only
+// on cnt (placement invariance).
 int chunk_tiles(int cnt, int P) {
+  static const int min_env = [] {   // development knob: PINN_DD_MIN_CHUNK_TILES
+    const char* e = std::getenv("PINN_DD_MIN_CHUNK_TILES");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
   const int tiles = (cnt + P - 1) / P;
-  return std::max(4, (tiles + 127) / 128);
+  const int min_tiles = min_env ? min_env : (tiles >= 200 ? 4 : 1);
+  return std::max(min_tiles, (tiles + 127) / 128);
 }
 
 // point counts of the K1 chunks of a run of `cnt` points: full chunks of
