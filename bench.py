@@ -247,11 +247,19 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # PINN_BENCH_SHARED_GPU=1: validation of the N > 1 code path on a one-GPU box
+    # (every rank on cuda:0, gloo, payloads staged through the host); the line it
+    # prints is marked and is never a bench number
+    shared = os.environ.get("PINN_BENCH_SHARED_GPU") == "1" and world > 1
+    gpu = 0 if shared else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
     # per-kernel CUDA events (FLAG_TIMING) only at N = 1, where they are graph
@@ -301,7 +309,7 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(gpu)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -406,6 +414,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
+            **({"shared_gpu_validation": "all ranks on cuda:0 over gloo: code-path check, not a bench number"}
+               if shared else {}),
             "iters_per_s": 1e3 * args.steps / t_max,
             "config": {"workload": f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}",
                        "subdomains": prob.n_sub,
