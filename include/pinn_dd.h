@@ -196,6 +196,14 @@ pinn_dd_status pinn_dd_adam(pinn_dd* h);
    J returns PINN_DD_ENONFINITE. */
 pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host);
 
+/* Stream-ordered copy of the loss breakdown [n_sub][8] (MSE_u, MSE_F,
+   MSE_uavg, MSE_if, J_q (Eq. 5/6), non-finite flag, 0, 0) of the last
+   loss+grad evaluation into dst (pinned host or device memory, caller-owned).
+   No synchronisation and no non-finite check (read the flag column, or call
+   pinn_dd_step with loss_host); lets a caller pipeline the per-step loss
+   read-back with the next step. */
+pinn_dd_status pinn_dd_read_loss(pinn_dd* h, float* dst);
+
 /* K6: Eq. (4) stitched solution u(z) = sum_q u_q(z) 1_{Omega_q}(z) with weight
    1/S at points shared by S subdomains.  pts: device [2][n]; owners: device
    [n][4] local subdomain ids (-1 = unused), the caller's point classification;

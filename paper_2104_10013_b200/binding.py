@@ -32,7 +32,7 @@ EXPORTS = [
     "pinn_dd_payload_buffer", "pinn_dd_loss_grad", "pinn_dd_loss_grad_interior", "pinn_dd_loss_grad_interface",
     "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict",
     "pinn_dd_get_params", "pinn_dd_set_params", "pinn_dd_get_step", "pinn_dd_kernel_times",
-    "pinn_dd_plan_info", "pinn_dd_step_fused", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
+    "pinn_dd_plan_info", "pinn_dd_step_fused", "pinn_dd_read_loss", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
 ]
 
 
@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH):
     lib.pinn_dd_get_step.argtypes = [vp, i32, C.POINTER(i32)]
     lib.pinn_dd_kernel_times.argtypes = [vp, C.POINTER(C.c_double)]
     lib.pinn_dd_plan_info.argtypes = [vp, C.POINTER(i64)]
+    lib.pinn_dd_read_loss.argtypes = [vp, vp]
     lib.pinn_dd_step_fused.argtypes = [vp]
     lib.pinn_dd_step_fused.restype = i32
     lib.pinn_dd_debug_buffer.argtypes = [vp, i32, C.POINTER(vp), C.POINTER(i64)]
@@ -388,6 +389,12 @@ class PinnDD:
         t = C.c_int32()
         self._check(self.lib.pinn_dd_get_step(self.h, q, C.byref(t)))
         return t.value
+
+    def read_loss(self, dst: torch.Tensor):
+        """Enqueue the copy of the last [n_sub, 8] loss breakdown into dst (pinned
+        host or device tensor) on the handle's stream; no synchronisation."""
+        assert dst.dtype == torch.float32 and dst.is_contiguous() and dst.numel() >= self.n_sub * 8
+        self._check(self.lib.pinn_dd_read_loss(self.h, C.c_void_p(dst.data_ptr())))
 
     @property
     def step_fused(self) -> bool:

@@ -1013,6 +1013,12 @@ pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4) {
   return PINN_DD_OK;
 }
 
+pinn_dd_status pinn_dd_read_loss(pinn_dd* h, float* dst) {
+  if (!h || !dst) return fail(h, PINN_DD_EINVAL, "bad read_loss arguments");
+  CK(h, cudaMemcpyAsync(dst, h->loss, size_t(h->d.n_sub) * 8 * 4, cudaMemcpyDefault, h->stream));
+  return PINN_DD_OK;
+}
+
 int32_t pinn_dd_step_fused(const pinn_dd* h) { return h && use_fused(h) ? 1 : 0; }
 
 pinn_dd_status pinn_dd_plan_info(pinn_dd* h, int64_t* info4) {
