@@ -34,6 +34,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
@@ -329,11 +331,15 @@ def run_ours(args):
     kt = h.kernel_times()                                  # K2, K1, K5 ms over the timed steps, launches
     t_local = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     pts_all = torch.tensor([pts_local], dtype=torch.float64, device=dev)
+    res_loc = torch.tensor([float(sum(len(h_prob.subdomains[q].x_f) for q in local))], dtype=torch.float64,
+                           device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
         dist.all_reduce(pts_all, op=dist.ReduceOp.SUM)
+        dist.all_reduce(res_loc, op=dist.ReduceOp.SUM)
     t_max = float(t_local.item())
     value = float(pts_all.item()) * args.steps / (t_max * 1e-3)
+    res_all = float(res_loc.item())
 
     # ---- end to end through the public API with host buffers (pinned H2D + D2H loss)
     host = [h.coords.cpu().pin_memory(), h.target.cpu().pin_memory(), h.mask.cpu().pin_memory()]
@@ -457,6 +463,9 @@ def run_ours(args):
             **({"shared_gpu_validation": "all ranks on cuda:0 over gloo: code-path check, not a bench number"}
                if shared else {}),
             "iters_per_s": 1e3 * args.steps / t_max,
+            "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
+                        "p90": float(np.percentile(step_ms, 90))},
+            "residual_points_per_s": res_all * args.steps / (t_max * 1e-3),   # N_F only (the paper's count)
             "config": {"workload": f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}",
                        "subdomains": prob.n_sub,
                        "subdomains_per_gpu": len(local), "points_per_step": int(pts_all.item()),
