@@ -318,6 +318,25 @@ def test_fused_step_equals_phased_calls(cfg, kw):
     b.close()
 
 
+def test_read_loss_async_matches_step_loss():
+    """pinn_dd_read_loss (stream-ordered, no sync) into pinned host and device
+    tensors returns the breakdown pinn_dd_step reports."""
+    prob = make_config("C1", n_f=300, n_i=30, n_u=40)
+    a = _handle(prob)
+    b = _handle(prob)
+    out = a.step(2)
+    b.step(2, want_loss=False)
+    host = torch.empty(prob.n_sub, 8).pin_memory()
+    dev = torch.empty(prob.n_sub, 8, device="cuda:0")
+    b.read_loss(host)
+    b.read_loss(dev)
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), out)
+    assert np.array_equal(dev.cpu().numpy(), out)
+    a.close()
+    b.close()
+
+
 def test_placement_invariance_two_handles():
     """Same decomposition as one handle or split over two 'ranks' (payload rows
     moved by the exchange plan): losses and gradients are bitwise equal."""
