@@ -105,11 +105,14 @@ struct KCfg {
   static constexpr int oU = oBuf + 2 * BUF;                // [P][DO] float4
   static constexpr int oX = oU + P * DO * 4;               // [2][P]
   static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [8 warps][4]
-  static constexpr int oDw = oRed + 32;                    // dW/db split scratch (S>1)
-  static constexpr int SCR = (S > 1) ? S * NBLK * JB * IB + S * NJ * JB : 0;
-  static constexpr int oAcc = al4(oDw + SCR);              // per-chunk gradient accumulator
+  static constexpr int oDw = oRed + 32;                    // dW/db scratch (split partials / coalescing)
   static constexpr int ACC = Lay<N, NH, DO>::total();
-  static constexpr bool DW_SMEM = (size_t(al4(oAcc + ACC + 4)) * 4) <= SMEM_CAP;
+  static constexpr int SCR1 = S * NBLK * JB * IB + S * NJ * JB;
+  static constexpr bool DW_SMEM = (size_t(al4(al4(oDw + (S > 1 ? SCR1 : 0)) + ACC + 4)) * 4) <= SMEM_CAP;
+  // the scratch is needed for S > 1 (split partials) and, with the chunk
+  // accumulator in global memory, to coalesce the per-tile read-modify-write
+  static constexpr int SCR = (S > 1 || !DW_SMEM) ? SCR1 : 0;
+  static constexpr int oAcc = al4(oDw + SCR);              // per-chunk gradient accumulator
   static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 4);   // + tmem address slot
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= SMEM_CAP, "shared memory budget");

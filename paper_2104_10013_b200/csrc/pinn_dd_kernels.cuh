@@ -220,7 +220,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
     for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = acc2[jj][ii].x + acc2[jj][ii].y;
-    if constexpr (S == 1) {
+    if constexpr (S == 1 && DWS) {
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
@@ -251,9 +251,10 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
   using C = KCfg<N, NH, DO, T>;
   constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
   constexpr int DBOFF = S * NBLK * JB * IB;
-  if constexpr (S > 1 && !DWS) {
-    // global accumulator: thread e owns dW entries e, e + T, ... (coalesced),
-    // all loads of the chunk partial issued before any store (one L2 round trip)
+  if constexpr (!DWS) {
+    // global accumulator: thread e owns dW entries e, e + T, ... (coalesced; the
+    // dW block mapping would touch 32 cache lines per warp access), all loads
+    // of the chunk partial issued before any store (one L2 round trip)
     const int tid = threadIdx.x;
     constexpr int NE = N * N, IT = (NE + T - 1) / T;
     float v[IT];
