@@ -304,10 +304,18 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
         v[it] = x;
       }
     }
+    // the entries are distinct: all accumulator loads first, then the stores
+    // (acc_add one by one serialised every load behind the previous store)
+    float cur[IT];
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int e = tid + it * T;
-      if (e < NE) acc_add<DWS>(accW, off[it], v[it], first);
+      if (e < NE) cur[it] = accW[off[it]];
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      if (e < NE) accW[off[it]] = cur[it] + v[it];
     }
     if (tid < N) {
       const int jb = tid % NJ, jj = tid / NJ;
