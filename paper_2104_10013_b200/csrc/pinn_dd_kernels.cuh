@@ -221,13 +221,19 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = acc2[jj][ii].x + acc2[jj][ii].y;
     if constexpr (S == 1 && DWS) {
+      // shared chunk accumulator, entries private to this thread: loads first
+      float cur[JB][IB], curb[JB];
 #pragma unroll
-      for (int jj = 0; jj < JB; ++jj)
+      for (int jj = 0; jj < JB; ++jj) {
 #pragma unroll
-        for (int ii = 0; ii < IB; ++ii) acc_add<DWS>(accW, (jb + NJ * jj) * N + ib + NI * ii, acc[jj][ii], first);
-      if (ib == 0) {
+        for (int ii = 0; ii < IB; ++ii) cur[jj][ii] = accW[(jb + NJ * jj) * N + ib + NI * ii];
+        curb[jj] = ib == 0 ? accB[jb + NJ * jj] : 0.0f;
+      }
 #pragma unroll
-        for (int jj = 0; jj < JB; ++jj) acc_add<DWS>(accB, jb + NJ * jj, db[jj], first);
+      for (int jj = 0; jj < JB; ++jj) {
+#pragma unroll
+        for (int ii = 0; ii < IB; ++ii) accW[(jb + NJ * jj) * N + ib + NI * ii] = cur[jj][ii] + acc[jj][ii];
+        if (ib == 0) accB[jb + NJ * jj] = curb[jj] + db[jj];
       }
     } else {
 #pragma unroll
