@@ -107,7 +107,11 @@ struct KCfg {
   static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [8 warps][4]
   static constexpr int oDw = oRed + 32;                    // dW/db scratch (split partials / coalescing)
   static constexpr int ACC = Lay<N, NH, DO>::total();
-  static constexpr int SCR1 = S * NBLK * JB * IB + S * NJ * JB;
+  // scratch: split s holds dW^k as [j][N + 1] (row padding spreads the dW-block
+  // writers over the banks; readers walk rows contiguously) then db^k [N]
+  static constexpr int SROW = N + 1;
+  static constexpr int SSPL = N * SROW;                    // floats per split (W part)
+  static constexpr int SCR1 = S * SSPL + S * N;
   static constexpr bool DW_SMEM = (size_t(al4(al4(oDw + (S > 1 ? SCR1 : 0)) + ACC + 4)) * 4) <= SMEM_CAP;
   // the scratch is needed for S > 1 (split partials) and, with the chunk
   // accumulator in global memory, to coalesce the per-tile read-modify-write

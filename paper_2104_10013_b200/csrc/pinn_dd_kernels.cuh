@@ -185,7 +185,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
   using C = KCfg<N, NH, DO, T>;
   constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
   constexpr int PS = C::P / S;
-  constexpr int DBOFF = S * NBLK * JB * IB;
+  constexpr int DBOFF = S * C::SSPL;
   const int tid = threadIdx.x;
   if (tid < NBLK * S) {
     const int r = tid % NBLK, s = tid / NBLK;
@@ -239,10 +239,10 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
-        for (int ii = 0; ii < IB; ++ii) sDw[(s * NBLK + r) * JB * IB + jj * IB + ii] = acc[jj][ii];
+        for (int ii = 0; ii < IB; ++ii) sDw[s * C::SSPL + (jb + NJ * jj) * C::SROW + ib + NI * ii] = acc[jj][ii];
       if (ib == 0) {
 #pragma unroll
-        for (int jj = 0; jj < JB; ++jj) sDw[DBOFF + (s * NJ + jb) * JB + jj] = db[jj];
+        for (int jj = 0; jj < JB; ++jj) sDw[DBOFF + s * N + jb + NJ * jj] = db[jj];
       }
     }
   }
@@ -255,12 +255,13 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 template <int N, int NH, int DO, int T, bool DWS>
 __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool first, const float* sDw) {
   using C = KCfg<N, NH, DO, T>;
-  constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
-  constexpr int DBOFF = S * NBLK * JB * IB;
-  if constexpr (!DWS) {
-    // global accumulator: thread e owns dW entries e, e + T, ... (coalesced; the
-    // dW block mapping would touch 32 cache lines per warp access), all loads
-    // of the chunk partial issued before any store (one L2 round trip)
+  constexpr int S = C::S;
+  constexpr int DBOFF = S * C::SSPL;
+  if constexpr (!DWS || S > 1) {
+    // thread e owns dW entries e, e + T, ... in natural [j][i] order: the
+    // scratch rows, the shared accumulator and the global partial are all read
+    // contiguously (no bank conflicts, coalesced); every load is issued before
+    // any store (the entries are distinct).  Split order s = 0 .. S-1.
     const int tid = threadIdx.x;
     constexpr int NE = N * N, IT = (NE + T - 1) / T;
     float v[IT];
@@ -269,66 +270,29 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
       const int e = tid + it * T;
       if (e < NE) {
         const int j = e / N, i = e - (e / N) * N;
-        const int r = (j % NJ) + NJ * (i % NI);
-        const float* src = sDw + r * JB * IB + (j / NJ) * IB + (i / NI);
+        const float* src = sDw + j * C::SROW + i;
         float x = src[0];
 #pragma unroll
-        for (int s = 1; s < S; ++s) x += src[s * NBLK * JB * IB];
-        v[it] = first ? x : accW[e] + x;
-      }
-    }
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int e = tid + it * T;
-      if (e < NE) accW[e] = v[it];
-    }
-    if (tid < N) {
-      const int jb = tid % NJ, jj = tid / NJ;
-      float x = 0.0f;
-#pragma unroll
-      for (int s = 0; s < S; ++s) x += sDw[DBOFF + (s * NJ + jb) * JB + jj];
-      accB[tid] = first ? x : accB[tid] + x;
-    }
-  } else if constexpr (S > 1) {
-    // shared accumulator: entry e = (block r, row jj, column ii) of the split
-    // scratch is contiguous in e, so thread e's S loads are conflict-free; all
-    // loads are issued before any store (one shared-memory round trip)
-    const int tid = threadIdx.x;
-    constexpr int NE = NBLK * JB * IB, IT = (NE + T - 1) / T;
-    float v[IT];
-    int off[IT];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int e = tid + it * T;
-      if (e < NE) {
-        float x = sDw[e];
-#pragma unroll
-        for (int s = 1; s < S; ++s) x += sDw[s * NE + e];
-        const int r = e / (JB * IB), rem = e - r * (JB * IB);
-        const int jj = rem / IB, ii = rem - jj * IB;
-        off[it] = ((r % NJ) + NJ * jj) * N + (r / NJ) + NI * ii;
+        for (int s = 1; s < S; ++s) x += src[s * C::SSPL];
         v[it] = x;
       }
     }
-    // the entries are distinct: all accumulator loads first, then the stores
-    // (acc_add one by one serialised every load behind the previous store)
     float cur[IT];
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int e = tid + it * T;
-      if (e < NE) cur[it] = accW[off[it]];
+      if (e < NE) cur[it] = (DWS || !first) ? accW[e] : 0.0f;
     }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int e = tid + it * T;
-      if (e < NE) accW[off[it]] = cur[it] + v[it];
+      if (e < NE) accW[e] = (DWS || !first) ? cur[it] + v[it] : v[it];
     }
     if (tid < N) {
-      const int jb = tid % NJ, jj = tid / NJ;
       float x = 0.0f;
 #pragma unroll
-      for (int s = 0; s < S; ++s) x += sDw[DBOFF + (s * NJ + jb) * JB + jj];
-      acc_add<DWS>(accB, tid, x, first);
+      for (int s = 0; s < S; ++s) x += sDw[DBOFF + s * N + tid];
+      accB[tid] = (DWS || !first) ? accB[tid] + x : x;
     }
   }
 }
