@@ -79,6 +79,13 @@ struct KCfg {
   static constexpr int P = T / NB;             // points per tile (1 point per thread)
   static constexpr int CPS = 256 / T;          // CTAs per SM
   static constexpr int PSTR = P + 1;           // float4 row stride of activation buffers (odd)
+  // float4 skew per block of kJT rows: for NB = 2 (width 20) the 8 lanes of a
+  // 128-bit store phase (2 neuron blocks x 4 points) then hit 8 distinct 16-B
+  // bank groups instead of 2-way conflicts (C3 K1 0.284 -> 0.269 ms).  For
+  // NB = 8 the analogous skew (7) slowed 5x80 down (17.97 vs 16.53 ms: it
+  // moves the dW-block row reads onto shared banks), so it stays 0 there.
+  static constexpr int SKW = NB == 2 ? ((4 - (kJT * PSTR) % 8) % 8 + 8) % 8 : 0;
+  __host__ __device__ static constexpr int row(int j) { return j * PSTR + (j / kJT) * SKW; }
   // W^k (k = 2..NH) rows: j*WS + (j/kJT)*4 floats (block skew against bank conflicts)
   static constexpr int WS = al4(N);
   static constexpr int WROWS = N * WS + NB * 4;            // floats per hidden W in smem
@@ -101,7 +108,7 @@ struct KCfg {
   static constexpr int oBo = oWo + DO * WS;                // [DO]
   static constexpr int oSl = al4(oBo + DO);                // [NH] slopes s_k = n a^k
   static constexpr int oBuf = al4(oSl + NH) ;              // 2 x [N][PSTR] float4
-  static constexpr int BUF = N * PSTR * 4;
+  static constexpr int BUF = (row(N - 1) + PSTR) * 4;     // floats per activation buffer
   static constexpr int oU = oBuf + 2 * BUF;                // [P][DO] float4
   static constexpr int oX = oU + P * DO * 4;               // [2][P]
   static constexpr int oRed = al4(oX + 2 * P);             // reduction scratch [8 warps][4]

@@ -137,7 +137,7 @@ __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const f
   for (int i = 0; i < N; i += 4) {
     float4 h[4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) h[m] = Hin[(i + m) * C::PSTR + pg];
+    for (int m = 0; m < 4; ++m) h[m] = Hin[C::row(i + m) + pg];
     float4 w[kJT];
 #pragma unroll
     for (int jj = 0; jj < kJT; ++jj) w[jj] = *reinterpret_cast<const float4*>(Wb + jj * C::WS + i);
@@ -161,7 +161,7 @@ __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const fl
   for (int jb = 0; jb < C::NB; ++jb) {
     // rows jb*kJT .. +kJT-1 share the block skew jb*4
     const float* Wrow = W + jb * (kJT * C::WS + 4) + j0;
-    const float4* Zrow = Zb + jb * kJT * C::PSTR + pg;
+    const float4* Zrow = Zb + C::row(jb * kJT) + pg;   // rows of one block share its skew
 #pragma unroll
     for (int jj = 0; jj < kJT; ++jj) {
       const float4 zb = Zrow[jj * C::PSTR];
@@ -202,9 +202,9 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
     for (int p = s * PS; p < (s + 1) * PS; ++p) {
       float4 zr[JB], hr[IB];
 #pragma unroll
-      for (int jj = 0; jj < JB; ++jj) zr[jj] = Zb[(jb + NJ * jj) * C::PSTR + p];
+      for (int jj = 0; jj < JB; ++jj) zr[jj] = Zb[C::row(jb + NJ * jj) + p];
 #pragma unroll
-      for (int ii = 0; ii < IB; ++ii) hr[ii] = H[(ib + NI * ii) * C::PSTR + p];
+      for (int ii = 0; ii < IB; ++ii) hr[ii] = H[C::row(ib + NI * ii) + p];
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   const float* sBo = sm + C::oBo;
   const float* sSl = sm + C::oSl;
   float4* buf0 = reinterpret_cast<float4*>(sm + C::oBuf);
-  float4* buf1 = buf0 + N * C::PSTR;
+  float4* buf1 = buf0 + C::BUF / 4;
   float4* sU = reinterpret_cast<float4*>(sm + C::oU);
   float* sX = sm + C::oX;
   float* sY = sX + C::P;
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
           if constexpr (MS == 0) st.store(0, reinterpret_cast<const float*>(z));
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) buf0[(j0 + jj) * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
+          for (int jj = 0; jj < kJT; ++jj) buf0[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
         }
         cta_sync();
 #pragma unroll 1
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
           if constexpr (MS == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) Hout[(j0 + jj) * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
+          for (int jj = 0; jj < kJT; ++jj) Hout[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
           cta_sync();
         }
         const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           const float* w = sWo + o * C::WS;
 #pragma unroll 4
           for (int i = 0; i < N; ++i) {
-            const float4 h = HL[i * C::PSTR + p];
+            const float4 h = HL[C::row(i) + p];
             const float wi = w[i];
             acc.x = fmaf(wi, h.x, acc.x);
             acc.y = fmaf(wi, h.y, acc.y);
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             float acc = 0.0f;
 #pragma unroll 4
             for (int p = qq; p < C::P; p += 4) {
-              const float4 h = HL[i * C::PSTR + p];
+              const float4 h = HL[C::row(i) + p];
               const float4 ub = sU[p * DO + o];
               acc = fmaf(h.x, ub.x, fmaf(h.y, ub.y, fmaf(h.z, ub.z, fmaf(h.w, ub.w, acc))));
             }
@@ -635,8 +635,8 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           cta_sync();
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
-            bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
-            if (NH >= 2) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
+            bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
+            if (NH >= 2) bufH[C::row(j0) + jj * C::PSTR + pg] = z[jj];
           }
           cta_sync();
 #pragma unroll 1
@@ -660,8 +660,8 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
 #pragma unroll
             for (int jj = 0; jj < kJT; ++jj) {
-              bufZ[(j0 + jj) * C::PSTR + pg] = hb[jj];
-              if (more) bufH[(j0 + jj) * C::PSTR + pg] = z[jj];
+              bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
+              if (more) bufH[C::row(j0) + jj * C::PSTR + pg] = z[jj];
             }
             cta_sync();
           }
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
 #pragma unroll 4
             for (int p = qq; p < C::P; p += 4) {
-              const float4 zb = bufZ[j * C::PSTR + p];
+              const float4 zb = bufZ[C::row(j) + p];
               a0 = fmaf(zb.x, sX[p], a0) + zb.y;
               a1 = fmaf(zb.x, sY[p], a1) + zb.z;
               ab += zb.x;
