@@ -191,17 +191,26 @@ template <int ACT>
 __device__ __forceinline__ float stash_x(float zx, float s, int act = ACT) {
   return act_sel<ACT>(act) == 0 ? tanhf(s * zx) : zx;
 }
+// Scaled derivatives of the activation at u = s z from the stash form x:
+// d0 = sigma, c1 = s sigma', p2 = s^2 sigma'', r3 = s^3 sigma^(3).  For tanh
+// (x = t) they are polynomials in t: sigma' = 1 - t^2 =: a, sigma'' = -2 t a,
+// sigma^(3) = a (6 t^2 - 2) = a (4 - 6 a).
 template <int ACT>
-__device__ __forceinline__ void derivs_from_stash(float x, float s, float& s0, float& s1, float& s2, float& s3,
-                                                  int act = ACT) {
+__device__ __forceinline__ void scaled_derivs(float x, float s, float& d0, float& c1, float& p2, float& r3,
+                                              int act = ACT) {
   if (act_sel<ACT>(act) == 0) {
-    const float t = x;
-    s0 = t;
-    s1 = 1.0f - t * t;
-    s2 = -2.0f * t * s1;
-    s3 = s1 * (6.0f * t * t - 2.0f);
+    const float a = fmaf(-x, x, 1.0f);
+    d0 = x;
+    c1 = s * a;
+    p2 = (x * a) * (-2.0f * s * s);
+    r3 = (a * (s * s * s)) * fmaf(-6.0f, a, 4.0f);
   } else {
+    float s0, s1, s2, s3;
     act_derivs<ACT>(s * x, s0, s1, s2, s3, act);
+    d0 = s0;
+    c1 = s * s1;
+    p2 = (s * s) * s2;
+    r3 = (s * s * s) * s3;
   }
 }
 
@@ -209,16 +218,10 @@ __device__ __forceinline__ void derivs_from_stash(float x, float s, float& s0, f
 // h = (sigma, sigma' s g1, sigma' s g2, sigma'' s^2 Q + sigma' s L)
 template <int ACT>
 __device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2, int act = ACT) {
-  float s0, s1, s2, s3;
-  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3, act);
-  const float Q = m1 * z.y * z.y + m2 * z.z * z.z;
-  const float ss = s1 * s;
-  float4 h;
-  h.x = s0;
-  h.y = ss * z.y;
-  h.z = ss * z.z;
-  h.w = s2 * s * s * Q + ss * z.w;
-  return h;
+  float d0, c1, p2, r3;
+  scaled_derivs<ACT>(z.x, s, d0, c1, p2, r3, act);
+  const float Q = fmaf(m2 * z.z, z.z, (m1 * z.y) * z.y);
+  return make_float4(d0, c1 * z.y, c1 * z.z, fmaf(p2, Q, c1 * z.w));
 }
 
 // adjoint of act_fwd: given hb = dJ/dh (4 channels) and the stash form of the
@@ -226,16 +229,18 @@ __device__ __forceinline__ float4 act_fwd(float4 z, float s, float m1, float m2,
 // NOT accumulated here: J depends on (s_k, W^k, b^k) only through s_k W^k and
 // s_k b^k, so a_k dJ/da_k = <W^k, dJ/dW^k> + <b^k, dJ/db^k> exactly; K5
 // evaluates that identity once per step.
+//   zb  = s sigma' hb_v + s^2 sigma'' (hb_1 g1 + hb_2 g2) + hb_L (s^3 sigma^(3) Q + s^2 sigma'' L)
+//   g1b = s sigma' hb_1 + 2 m1 hb_L s^2 sigma'' g1   (g2b likewise),   Lb = s sigma' hb_L
 template <int ACT>
 __device__ __forceinline__ float4 act_bwd(float4 z, float4 hb, float s, float m1, float m2, int act = ACT) {
-  float s0, s1, s2, s3;
-  derivs_from_stash<ACT>(z.x, s, s0, s1, s2, s3, act);
-  const float Q = m1 * z.y * z.y + m2 * z.z * z.z;
-  const float zb = hb.x * s1 + s * s2 * (hb.y * z.y + hb.z * z.z) + hb.w * (s3 * s * s * Q + s2 * s * z.w);
-  const float g1 = hb.y * s1 + 2.0f * m1 * hb.w * s2 * s * z.y;
-  const float g2 = hb.z * s1 + 2.0f * m2 * hb.w * s2 * s * z.z;
-  const float lb = hb.w * s1;
-  return make_float4(s * zb, s * g1, s * g2, s * lb);
+  float d0, c1, p2, r3;
+  scaled_derivs<ACT>(z.x, s, d0, c1, p2, r3, act);
+  const float Q = fmaf(m2 * z.z, z.z, (m1 * z.y) * z.y);
+  const float A = hb.w * p2;
+  const float zb = fmaf(c1, hb.x, fmaf(p2, fmaf(hb.z, z.z, hb.y * z.y), fmaf(A, z.w, hb.w * (r3 * Q))));
+  const float g1 = fmaf(c1, hb.y, (A * (2.0f * m1)) * z.y);
+  const float g2 = fmaf(c1, hb.z, (A * (2.0f * m2)) * z.z);
+  return make_float4(zb, g1, g2, c1 * hb.w);
 }
 
 // ----------------------------------------------------------------------------
