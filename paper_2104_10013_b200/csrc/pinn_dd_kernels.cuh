@@ -545,20 +545,25 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           cta_sync();
         }
         const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
-        for (int idx = tid; idx < C::P * DO; idx += T) {
+        // output layer: 4 lanes per (point, output), each over every 4th input,
+        // combined by a fixed xor-shuffle tree (short dependent chains)
+        static_assert((4 * C::P * DO) % 32 == 0, "warp-uniform trip count");
+        for (int t4 = tid; t4 < 4 * C::P * DO; t4 += T) {
+          const int qq = t4 & 3, idx = t4 >> 2;
           const int p = idx % C::P, o = idx / C::P;
-          float4 acc = make_float4(sBo[o], 0.0f, 0.0f, 0.0f);
+          float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
           const float* w = sWo + o * C::WS;
 #pragma unroll 4
-          for (int i = 0; i < N; ++i) {
-            const float4 h = HL[C::row(i) + p];
-            const float wi = w[i];
-            acc.x = fmaf(wi, h.x, acc.x);
-            acc.y = fmaf(wi, h.y, acc.y);
-            acc.z = fmaf(wi, h.z, acc.z);
-            acc.w = fmaf(wi, h.w, acc.w);
+          for (int i = qq; i < N; i += 4) fma4(acc, w[i], HL[C::row(i) + p]);
+#pragma unroll
+          for (int off = 1; off < 4; off <<= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
+            acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
           }
-          sU[p * DO + o] = acc;
+          acc.x += sBo[o];
+          if (qq == 0) sU[p * DO + o] = acc;
         }
         cta_sync();
 
@@ -591,13 +596,15 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           for (int t4 = tid; t4 < 4 * DO * N; t4 += T) {   // warp-uniform trip count
             const int qq = t4 & 3, idx = t4 >> 2;
             const int o = idx / N, i = idx % N;
-            float acc = 0.0f;
+            float2 a2 = make_float2(0.0f, 0.0f);   // channel pairs (x.x + z.z, y.y + w.w)
 #pragma unroll 4
             for (int p = qq; p < C::P; p += 4) {
               const float4 h = HL[C::row(i) + p];
               const float4 ub = sU[p * DO + o];
-              acc = fmaf(h.x, ub.x, fmaf(h.y, ub.y, fmaf(h.z, ub.z, fmaf(h.w, ub.w, acc))));
+              a2 = __ffma2_rn(make_float2(h.x, h.y), make_float2(ub.x, ub.y), a2);
+              a2 = __ffma2_rn(make_float2(h.z, h.w), make_float2(ub.z, ub.w), a2);
             }
+            float acc = a2.x + a2.y;
             acc += __shfl_xor_sync(__activemask(), acc, 1);
             acc += __shfl_xor_sync(__activemask(), acc, 2);
             if (qq == 0) acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
