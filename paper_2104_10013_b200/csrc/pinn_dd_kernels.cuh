@@ -389,7 +389,14 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   using LY = Lay<N, NH, DO>;
   extern __shared__ __align__(16) float sm[];
   const int tid = threadIdx.x;
-  const int nb = tid % C::NB, pg = tid / C::NB;
+  // thread -> (point group pg, neuron block nb).  With 8 neuron blocks the
+  // 8-lane phases of a 128-bit shared store hold 4 blocks x 2 points (lane
+  // bits 0,1,3 -> nb, bits 2,4 -> point), which makes the activation stores
+  // conflict-free (8 blocks x 1 point hit 4 bank groups twice); the loads see
+  // the same address sets per warp as before.
+  const int lane = tid & 31;
+  const int nb = C::NB == 8 ? ((lane & 3) | (((lane >> 3) & 1) << 2)) : tid % C::NB;
+  const int pg = C::NB == 8 ? ((tid >> 5) * 4 + (((lane >> 2) & 1) | ((lane >> 4) << 1))) : tid / C::NB;
   const int j0 = nb * kJT;
   const float* sW1 = sm + C::oW1;
   const float* sB1 = sm + C::oB1;
