@@ -215,28 +215,30 @@ pinn_dd_status fail(pinn_dd* h, pinn_dd_status s, const char* fmt, ...) {
 
 int n_eq_of(int pde) { return pde == PINN_DD_PDE_NS ? 3 : 1; }
 
-// tiles per chunk of a subdomain with `cnt` points: >= 4 tiles, <= ~128 chunks
-// Tiles per full chunk of a run of `cnt` points: at most ~128 chunks per run;
-// runs of >= 200 tiles use >= 4-tile chunks (fewer partial slots to flush and
-// reduce), shorter runs (the small C5 regions) 1-tile chunks so the persistent
-// schedule's tail stays one tile long (C5 K1 0.573 -> 0.531 ms).  Depends only
-// on cnt (placement invariance).
-int chunk_tiles(int cnt, int P) {
+// Tiles per full chunk of a run of `cnt` points: at most ~128 chunks per run.
+// Runs of >= 200 tiles use chunks of >= m tiles, m = ACC / 2048 clamped to
+// [1, 4] (ACC = floats of a chunk's gradient partial, flushed once per chunk
+// and read back by K5a: 6x40 -> 4, 5x20 -> 1, i.e. 3-tile chunks for C3's
+// 324-tile runs, K1 0.267 -> 0.260 ms); shorter runs (the small C5 regions)
+// 1-tile chunks so the persistent schedule's tail stays one tile long (C5 K1
+// 0.573 -> 0.531 ms).  Depends only on cnt and the net (placement invariance).
+int chunk_tiles(int cnt, int P, int acc) {
   static const int min_env = [] {   // development knob: PINN_DD_MIN_CHUNK_TILES
     const char* e = std::getenv("PINN_DD_MIN_CHUNK_TILES");
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
   const int tiles = (cnt + P - 1) / P;
-  const int min_tiles = min_env ? min_env : (tiles >= 200 ? 4 : 1);
+  const int m = std::min(4, std::max(1, acc / 2048));
+  const int min_tiles = min_env ? min_env : (tiles >= 200 ? m : 1);
   return std::max(min_tiles, (tiles + 127) / 128);
 }
 
 // point counts of the K1 chunks of a run of `cnt` points: full chunks of
 // chunk_tiles(cnt) tiles, the remainder as one-tile chunks (the schedule's
 // tail); depends only on cnt (placement invariance)
-void chunk_sizes(int cnt, int P, std::vector<int>& out) {
+void chunk_sizes(int cnt, int P, int acc, std::vector<int>& out) {
   if (cnt == 0) return;
-  const int span = chunk_tiles(cnt, P) * P;
+  const int span = chunk_tiles(cnt, P, acc) * P;
   int s0 = 0;
   for (; s0 + span <= cnt; s0 += span) out.push_back(span);
   for (; s0 < cnt; s0 += P) out.push_back(std::min(P, cnt - s0));
@@ -246,10 +248,10 @@ void chunk_sizes(int cnt, int P, std::vector<int>& out) {
 // interface points (a chunk never mixes the two, so the interface part can run
 // after the payload exchange); sign of the entry = interface run.
 // An empty subdomain still gets one (empty) chunk and thus a partial slot.
-std::vector<int> split_chunks(int na, int ni, int P) {
+std::vector<int> split_chunks(int na, int ni, int P, int acc) {
   std::vector<int> a, b;
-  chunk_sizes(na, P, a);
-  chunk_sizes(ni, P, b);
+  chunk_sizes(na, P, acc, a);
+  chunk_sizes(ni, P, acc, b);
   for (int& v : b) v = -v - 1;
   a.insert(a.end(), b.begin(), b.end());
   if (a.empty()) a.push_back(0);
@@ -361,7 +363,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   for (int q = 0; q < d->n_sub; ++q) {
     const int cnt = d->sub_point_offset[q + 1] - d->sub_point_offset[q];
     const int na = d->sub_n_res[q] + d->sub_n_data[q];
-    n1 += int(split_chunks(na, cnt - na, P).size());
+    n1 += int(split_chunks(na, cnt - na, P, ops->pstride).size());
     const int ni = cnt - d->sub_n_res[q] - d->sub_n_data[q];
     n2 += (ni + P - 1) / P;
   }
@@ -403,7 +405,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->total = c.off;
   if (h) {
     h->ops = ops;
-    h->tpc = chunk_tiles(d->n_sub ? d->sub_point_offset[1] - d->sub_point_offset[0] : 0, P);
+    h->tpc = chunk_tiles(d->n_sub ? d->sub_point_offset[1] - d->sub_point_offset[0] : 0, P, ops->pstride);
     h->n_chunks1 = n1;
     h->n_chunks2 = n2;
     h->grid1 = grid1;
@@ -739,7 +741,7 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
     const int off = h->sub_off[q], cnt = h->sub_off[q + 1] - off;
     const int na = h->n_res[q] + h->n_data[q];
     int s0 = 0;
-    for (int sz : split_chunks(na, cnt - na, P)) {
+    for (int sz : split_chunks(na, cnt - na, P, h->ops->pstride)) {
       const bool iface = sz < 0;
       if (iface) sz = -sz - 1;
       c1.push_back(Chunk{q, off + s0, sz, iface ? 1 : 0});
