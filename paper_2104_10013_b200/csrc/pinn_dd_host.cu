@@ -139,9 +139,11 @@ const Ops* find_ops(int N, int NH, int DO, int ACT, int pt = -1) {
       // width 20: two 128-thread CTAs per SM (C3 K1 0.369 -> 0.285 ms)
       Inst<20, 3, 1, 0, false, 128>::ops(),  Inst<20, 5, 1, 0, false, 128>::ops(),
       Inst<20, 3, 1, 0>::ops(),              Inst<20, 5, 1, 0>::ops(),
-      // widths 40 / 80: one 256-thread CTA per SM (the 128-thread 6x40 CTA is slower: 1.65 vs 1.55 ms)
-      Inst<40, 6, 1, 0>::ops(),              Inst<80, 5, 3, 0>::ops(),
-      Inst<80, 3, 2, kActMixed>::ops(),      Inst<40, 6, 1, 0, false, 128>::ops(),
+      // width 40: two 128-thread CTAs per SM as well (C2 K1 1.443 -> 1.423 ms since the
+      // coalesced chunk-partial read-modify-write; it was 1.65 vs 1.55 ms before)
+      Inst<40, 6, 1, 0, false, 128>::ops(),  Inst<40, 6, 1, 0>::ops(),
+      // width 80: one 256-thread CTA per SM (the weights alone are 104 KB of shared memory)
+      Inst<80, 5, 3, 0>::ops(),              Inst<80, 3, 2, kActMixed>::ops(),
   };
   // development knob: PINN_DD_CTA_THREADS=128|256 picks the CTA size where both exist
   const char* ev = std::getenv("PINN_DD_CTA_THREADS");
@@ -215,7 +217,8 @@ pinn_dd_status fail(pinn_dd* h, pinn_dd_status s, const char* fmt, ...) {
 
 int n_eq_of(int pde) { return pde == PINN_DD_PDE_NS ? 3 : 1; }
 
-// Tiles per full chunk of a run of `cnt` points: at most ~128 chunks per run.
+// Tiles per full chunk of a run of `cnt` points: at most ~128 chunks per run
+// (1024 for giant runs, below).
 // Runs of >= 200 tiles use chunks of >= m tiles, m = ACC / 2048 clamped to
 // [1, 4] (ACC = floats of a chunk's gradient partial, flushed once per chunk
 // and read back by K5a: 6x40 -> 4, 5x20 -> 1, i.e. 3-tile chunks for C3's
@@ -230,7 +233,11 @@ int chunk_tiles(int cnt, int P, int acc) {
   const int tiles = (cnt + P - 1) / P;
   const int m = std::min(4, std::max(1, acc / 2048));
   const int min_tiles = min_env ? min_env : (tiles >= 200 ? m : 1);
-  return std::max(min_tiles, (tiles + 127) / 128);
+  // a giant run (the data-parallel comparator's single subdomain: 7,530 tiles
+  // of 32) would get only ~128 chunks -- fewer than the persistent CTAs -- so
+  // runs of > 2048 tiles with partials of <= 64 KB may use up to 1024 chunks
+  const int max_chunks = (tiles > 2048 && acc <= 16384) ? 1024 : 128;
+  return std::max(min_tiles, (tiles + max_chunks - 1) / max_chunks);
 }
 
 // point counts of the K1 chunks of a run of `cnt` points: full chunks of
