@@ -252,11 +252,37 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 // order into the accumulator.  Called after the CTA barrier that follows
 // gemm_bwd, so it needs no barrier of its own and its shared-memory latency
 // overlaps the activation-buffer stores that follow.
+// Global chunk partial (!DWS) with few entries per thread: its current values
+// are loaded right after gemm_dw (before gemm_bwd and the barrier), so the L2
+// round trip overlaps the input-adjoint GEMM instead of following the barrier.
 template <int N, int NH, int DO, int T, bool DWS>
-__device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool first, const float* sDw) {
+struct DwPre {
+  static constexpr int IT = (N * N + T - 1) / T;
+  static constexpr bool ON = !DWS && IT <= 16;
+};
+
+template <int N, int NH, int DO, int T, bool DWS>
+__device__ __forceinline__ void gemm_dw_prefetch(const float* accW, const float* accB, bool first, float* pre,
+                                                 float& preb) {
+  if constexpr (DwPre<N, NH, DO, T, DWS>::ON) {
+    constexpr int NE = N * N, IT = DwPre<N, NH, DO, T, DWS>::IT;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      pre[it] = (!first && e < NE) ? __ldcg(accW + e) : 0.0f;
+    }
+    preb = (!first && tid < N) ? __ldcg(accB + tid) : 0.0f;
+  }
+}
+
+template <int N, int NH, int DO, int T, bool DWS>
+__device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool first, const float* sDw,
+                                               const float* pre, float preb) {
   using C = KCfg<N, NH, DO, T>;
   constexpr int S = C::S;
   constexpr int DBOFF = S * C::SSPL;
+  constexpr bool PRE = DwPre<N, NH, DO, T, DWS>::ON;
   if constexpr (!DWS || S > 1) {
     // thread e owns dW entries e, e + T, ... in natural [j][i] order: the
     // scratch rows, the shared accumulator and the global partial are all read
@@ -281,7 +307,10 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int e = tid + it * T;
-      if (e < NE) cur[it] = (DWS || !first) ? accW[e] : 0.0f;
+      if constexpr (PRE)
+        cur[it] = pre[it];
+      else if (e < NE)
+        cur[it] = (DWS || !first) ? accW[e] : 0.0f;
     }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
@@ -292,7 +321,10 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
       float x = 0.0f;
 #pragma unroll
       for (int s = 0; s < S; ++s) x += sDw[DBOFF + s * N + tid];
-      accB[tid] = (DWS || !first) ? accB[tid] + x : x;
+      if constexpr (PRE)
+        accB[tid] = first ? x : preb + x;
+      else
+        accB[tid] = (DWS || !first) ? accB[tid] + x : x;
     }
   }
 }
@@ -657,6 +689,8 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           for (int k = NH; k >= 2; --k) {
             // dW^k, db^k
             gemm_dw<N, NH, DO, T, DSM, kUfDw>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
+            float pre[DwPre<N, NH, DO, T, DSM>::IT], preb = 0.0f;
+            gemm_dw_prefetch<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, pre, preb);
             // adjoint of H^{k-1}, then of Z^{k-1}
             gemm_bwd<N, NH, DO, T>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
             st.load(k - 2, reinterpret_cast<float*>(z));
@@ -671,7 +705,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
               for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
             }
             cta_sync();
-            gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw);
+            gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw, pre, preb);
 #pragma unroll
             for (int jj = 0; jj < kJT; ++jj) {
               bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
