@@ -20,6 +20,9 @@ namespace pinn {
 
 // unroll factors of the GEMM loops (i-quads forward, 10-row blocks of the input
 // adjoint, points of dW); overridable at build time for variant sweeps
+#ifndef PINN_DWPRE_MAX
+#define PINN_DWPRE_MAX 32
+#endif
 #ifndef PINN_UF_FWD
 #define PINN_UF_FWD 10
 #endif
@@ -258,7 +261,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 template <int N, int NH, int DO, int T, bool DWS>
 struct DwPre {
   static constexpr int IT = (N * N + T - 1) / T;
-  static constexpr bool ON = !DWS && IT <= 16;
+  static constexpr bool ON = !DWS && IT <= PINN_DWPRE_MAX;
 };
 
 template <int N, int NH, int DO, int T, bool DWS>
