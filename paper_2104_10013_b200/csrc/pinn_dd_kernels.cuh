@@ -638,6 +638,8 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           for (int t4 = tid; t4 < 4 * DO * N; t4 += T) {   // warp-uniform trip count
             const int qq = t4 & 3, idx = t4 >> 2;
             const int o = idx / N, i = idx % N;
+            // global chunk partial: its current value is loaded before the dot product
+            const float prev = (!DSM && qq == 0 && !first) ? __ldcg(A + LY::offW(NH + 1) + idx) : 0.0f;
             float2 a2 = make_float2(0.0f, 0.0f);   // channel pairs (x.x + z.z, y.y + w.w)
 #pragma unroll 4
             for (int p = qq; p < C::P; p += 4) {
@@ -649,7 +651,12 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             float acc = a2.x + a2.y;
             acc += __shfl_xor_sync(__activemask(), acc, 1);
             acc += __shfl_xor_sync(__activemask(), acc, 2);
-            if (qq == 0) acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
+            if (qq == 0) {
+              if constexpr (DSM)
+                acc_add<DSM>(A, LY::offW(NH + 1) + idx, acc, first);
+              else
+                A[LY::offW(NH + 1) + idx] = first ? acc : prev + acc;
+            }
           }
           if (tid < DO) {
             float acc = 0.0f;
@@ -719,6 +726,10 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
           for (int t4 = tid; t4 < 4 * N; t4 += T) {
             const int qq = t4 & 3, j = t4 >> 2;
+            const bool pf = !DSM && qq == 0 && !first;   // global partial: load before the sums
+            const float p0 = pf ? __ldcg(A + LY::offW(1) + 2 * j) : 0.0f;
+            const float p1 = pf ? __ldcg(A + LY::offW(1) + 2 * j + 1) : 0.0f;
+            const float pb = pf ? __ldcg(A + LY::offB(1) + j) : 0.0f;
             float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
 #pragma unroll 4
             for (int p = qq; p < C::P; p += 4) {
@@ -735,9 +746,15 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
               ab += __shfl_xor_sync(mk, ab, o);
             }
             if (qq == 0) {
-              acc_add<DSM>(A, LY::offW(1) + 2 * j, a0, first);
-              acc_add<DSM>(A, LY::offW(1) + 2 * j + 1, a1, first);
-              acc_add<DSM>(A, LY::offB(1) + j, ab, first);
+              if constexpr (DSM) {
+                acc_add<DSM>(A, LY::offW(1) + 2 * j, a0, first);
+                acc_add<DSM>(A, LY::offW(1) + 2 * j + 1, a1, first);
+                acc_add<DSM>(A, LY::offB(1) + j, ab, first);
+              } else {
+                A[LY::offW(1) + 2 * j] = first ? a0 : p0 + a0;
+                A[LY::offW(1) + 2 * j + 1] = first ? a1 : p1 + a1;
+                A[LY::offB(1) + j] = first ? ab : pb + ab;
+              }
             }
           }
           // the slope entries of the partial stay 0 (K5 fills them)
