@@ -2,13 +2,17 @@
 """Benchmark of the parallel cPINN / XPINN training step (arXiv 2104.10013) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--method cpinn|xpinn]
+                    [--workload c4|c2|c3|c5] [--method cpinn|xpinn|hybrid|dp]
 
-Workload (BASELINE.json configs[1], "C2"): 2-D Poisson on [0, G] x [0, 1], a 4 x 4
-Cartesian block of subdomains per GPU (4G x 4 in total), 6 x 40 tanh networks,
-per subdomain 15000 residual + 80 boundary (boundary subdomains) + 250 per
-interface edge points.  G = 1 is exactly C2.  Each GPU owns one 4 x 4 block
-(weak scaling); cut-edge payloads move with torch.distributed P2P (NCCL).
+Default workload (BASELINE.json configs[3], "C4", the largest single-GPU
+config): 2-D steady incompressible Navier-Stokes (lid-driven cavity, Re 100)
+XPINN on a 4 x 2 decomposition of [0,1]^2, 5 x 80 tanh networks with outputs
+(u, v, p), 125,000 residual + 80 boundary + 250 per interface edge points per
+subdomain (1,005,640 points per step).  Strong scaling: the 8 subdomains are
+split into contiguous blocks, 8/N per GPU.  Other workloads: c2 (configs[1],
+Poisson 4x4 6x40, strong: 16/N subdomains per GPU), c3 (configs[2], Burgers
+x-t XPINN 5x20, weak: one 20k-point subdomain per GPU on a 1x1 / 2x1 / 2x2 /
+4x2 grid), c5 (configs[4], inverse heat on the 10-region map, LPT placement).
 
 A "step" = one synchronous Algorithm-1 iteration over every subdomain:
 interface payload (K2) -> [exchange] -> loss + gradient (K1, K5a) -> Adam (K5b).
@@ -70,6 +74,70 @@ def lpt_owner(loads, world):
         owner[q] = g
         tot[g] += loads[q]
     return owner
+
+
+def block_owner(prob, world):
+    """Contiguous Cartesian blocks of the subdomain grid, one per GPU, with the
+    block grid (gx, gy), gx * gy = world, that cuts the fewest edges (SURVEY
+    8(e): C2 at 8 GPUs -> 1 x 2 blocks, 16 of 24 edges cut)."""
+    nx, ny = prob.nx, prob.ny
+    best = None
+    for gx in range(1, world + 1):
+        if world % gx or nx % gx or ny % (world // gx):
+            continue
+        gy = world // gx
+        cut = (gx - 1) * ny + (gy - 1) * nx
+        if best is None or cut < best[0]:
+            best = (cut, gx, gy)
+    if best is None:
+        raise SystemExit(f"{prob.name}: {nx} x {ny} subdomains do not split into {world} blocks")
+    _, gx, gy = best
+    bx, by = nx // gx, ny // gy
+    return [(s.ix // bx) + gx * (s.iy // by) for s in prob.subdomains]
+
+
+def workload(name, method, world):
+    """(problem, owner per subdomain, scaling) of a bench workload at `world` GPUs."""
+    from pinn_inputs import make_config
+    if name == "c3":
+        prob = make_config("C3", method=method, gpus=world)        # one subdomain per GPU
+        return prob, list(range(prob.n_sub)), "weak"
+    if name == "c5":
+        prob = make_config("C5", method=method)
+        return prob, lpt_owner([prob.n_points(q) for q in range(prob.n_sub)], world), "strong"
+    prob = make_config(name.upper(), method=method)
+    return prob, block_owner(prob, world), "strong"
+
+
+def host_cpu():
+    """Host cores this process may use and the CPU model (lscpu)."""
+    cores = len(os.sched_getaffinity(0))
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return cores, model
+
+
+def algorithmic_bytes(prob, local, nf):
+    """HBM bytes one K1 launch must move at minimum: point coordinates (8 B),
+    targets + masks of data points (2 D_o x 4 B), payload rows read at
+    interface points (n_fields x 4 B), and per subdomain the parameters read
+    (4 B each; gradient partials are L2-resident)."""
+    P = prob.sizes
+    from pinn_inputs import n_params
+    b = 0
+    for q in local:
+        s = prob.subdomains[q]
+        ni = sum(len(prob.edges[e].pts) for e in s.edges)
+        b += 8 * (len(s.x_f) + len(s.x_u) + ni) + 8 * prob.d_out * len(s.x_u) + 4 * nf * ni
+        b += 4 * n_params(P)
+    return b
 
 
 def algorithmic_flops(prob, local):
@@ -149,17 +217,31 @@ class ClockSampler:
 # oracle legs (cpu_baseline and --impl reference)
 # --------------------------------------------------------------------------
 
-def oracle_sample_step(prob, st, q):
-    """Loss + gradient + Adam of subdomain q with its neighbours' payloads, FP64 oracle."""
+def sample_problem(prob, q, n_res):
+    """Subdomain q of `prob` with its residual points cut to the first n_res
+    (uniform i.i.d. samples, so any prefix is a uniform sample); its data and
+    interface points and every other subdomain unchanged."""
+    import dataclasses
+    s = prob.subdomains[q]
+    subs = list(prob.subdomains)
+    subs[q] = dataclasses.replace(s, x_f=s.x_f[:n_res])
+    return dataclasses.replace(prob, subdomains=subs)
+
+
+def oracle_sample_step(prob, st, q, n_res=None):
+    """Loss + gradient + Adam of subdomain q (residual points cut to n_res)
+    with its neighbours' payloads, FP64 oracle; returns the points processed."""
     from oracle import loss as OL
     import torch
+    if n_res is not None and n_res < len(prob.subdomains[q].x_f):
+        prob = sample_problem(prob, q, n_res)
     pay = {}
     for e in prob.subdomains[q].edges:
         nb = prob.edge_neighbor(q, e)
         ed = prob.edges[e]
         pay[(nb, e)] = OL.interface_payload(prob, st.thetas[nb].detach(),
                                             torch.as_tensor(ed.pts, dtype=torch.float64), ed.normal,
-                                            create_graph=False)
+                                            create_graph=False, q=nb)
     bd, g = OL.loss_and_grad(prob, q, st.thetas, pay)
     th, ad = OL.adam_step(st.thetas[q], g, st.adam[q], prob.lr, prob.beta1, prob.beta2, prob.eps)
     st.thetas[q] = th
@@ -167,24 +249,36 @@ def oracle_sample_step(prob, st, q):
     return prob.n_points(q)
 
 
+def oracle_sample_size(prob, seconds):
+    """Residual points per oracle sample step so that one step takes about
+    `seconds` (the FP64 oracle runs ~4-5 GFLOP/s on a 16-core host)."""
+    f = flops_per_point(prob.width, prob.n_hidden, prob.d_out)
+    return int(max(200, min(max(len(s.x_f) for s in prob.subdomains), seconds * 4e9 / f)))
+
+
 def cpu_baseline(prob, budget_s: float = 20.0):
-    """The oracle as it stands, on the host cores: full synchronous steps of the
-    whole decomposition until ~budget_s of CPU work (at least one step)."""
+    """The oracle as it stands, on the host cores: full synchronous steps of
+    the whole decomposition while they fit the budget, else loss + gradient +
+    Adam of single subdomains (cycling) on a bounded residual-point sample."""
     import torch
     from oracle import loss as OL
+    cores, model = host_cpu()
+    info = {"unit": UNIT, "cores": cores, "threads": torch.get_num_threads(), "cpu_model": model,
+            "kind": "oracle"}
     st = OL.init_state(prob)
-    if prob.n_points() > 300_000:
-        # too large for full oracle steps within the budget (C4: 1M points): time
-        # loss+grad+Adam of single subdomains (with their neighbours' payloads) instead
+    full_cost = flops_per_point(prob.width, prob.n_hidden, prob.d_out) * prob.n_points()
+    if full_cost > budget_s * 4e9:
+        n_res = oracle_sample_size(prob, 4.0)
         t0 = time.perf_counter()
         pts = k = 0
         while k == 0 or time.perf_counter() - t0 < budget_s:
-            pts += oracle_sample_step(prob, st, k % prob.n_sub)
+            pts += oracle_sample_step(prob, st, k % prob.n_sub, n_res)
             k += 1
         dt = time.perf_counter() - t0
-        return {"value": pts / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
-                "sample": f"{k} single-subdomain FP64 oracle step(s) of {prob.name} {prob.method} "
-                          f"({pts} pts), {dt:.1f} s"}
+        return {"value": pts / dt, **info,
+                "sample": f"{k} FP64 oracle loss+grad+Adam step(s) of single subdomains of {prob.name} "
+                          f"{prob.method} (cycling), residual points cut to {n_res} per subdomain, with the "
+                          f"neighbours' payloads ({pts} pts), {dt:.1f} s"}
     t0 = time.perf_counter()
     steps = 0
     while True:
@@ -194,7 +288,7 @@ def cpu_baseline(prob, budget_s: float = 20.0):
             break
     dt = time.perf_counter() - t0
     pts = prob.n_points() * steps
-    return {"value": pts / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
+    return {"value": pts / dt, **info,
             "sample": f"{steps} full FP64 oracle step(s) of {prob.name} {prob.method} "
                       f"({prob.n_sub} subdomains, {prob.n_points()} pts/step), {dt:.1f} s"}
 
@@ -204,30 +298,32 @@ def run_reference(args):
     if rank != 0:
         return
     import torch
-    from pinn_inputs import make_config
     from oracle import loss as OL
-    prob = (make_config("C2", method=args.method, weak=args.gpus) if args.workload == "c2"
-            else make_config(args.workload.upper(), method=args.method,
-                             **({"gpus": 8} if args.workload == "c3" else {})))
+    prob, owner, scaling = workload(args.workload, args.method, args.gpus)
+    # each step: one subdomain (cycling), residual points cut so that the whole
+    # --steps K --warmup W run stays within ~2 minutes
+    n_res = oracle_sample_size(prob, min(1.0, 120.0 / max(1, args.steps + args.warmup)))
     st = OL.init_state(prob)
     for w in range(args.warmup):
-        oracle_sample_step(prob, st, w % prob.n_sub)
+        oracle_sample_step(prob, st, w % prob.n_sub, n_res)
     t0 = time.perf_counter()
     pts = 0
     for k in range(args.steps):
-        pts += oracle_sample_step(prob, st, k % prob.n_sub)
+        pts += oracle_sample_step(prob, st, k % prob.n_sub, n_res)
     dt = time.perf_counter() - t0
     val = pts / dt
-    sample = (f"per step: loss+grad+Adam of ONE subdomain of {prob.name} {prob.method} (cycling), "
-              f"with its neighbours' payloads; {args.steps} steps, {pts} pts, {dt:.1f} s")
+    cores, model = host_cpu()
+    sample = (f"per step: FP64 oracle loss+grad+Adam of ONE subdomain of {prob.name} {prob.method} (cycling), "
+              f"residual points cut to {n_res}, with its neighbours' payloads; {args.steps} steps, {pts} pts, "
+              f"{dt:.1f} s")
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(1, args.steps), "higher_is_better": True,
-            "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{prob.name} {prob.method} (oracle sample)", "subdomains": prob.n_sub,
                        "net": f"2-{prob.width}x{prob.n_hidden}-{prob.d_out} tanh"},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "oracle",
-                             "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "threads": torch.get_num_threads(),
+                             "cpu_model": model, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -239,7 +335,6 @@ def run_reference(args):
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from pinn_inputs import make_config
     import __graft_entry__ as ge
     ge.build()
     from paper_2104_10013_b200.binding import PinnDD, FLAG_GRAPH, FLAG_TIMING
@@ -249,86 +344,73 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
-    # PINN_BENCH_SHARED_GPU=1: validation of the N > 1 code path on a one-GPU box
-    # (every rank on cuda:0, gloo, payloads staged through the host); the line it
-    # prints is marked and is never a bench number
-    shared = os.environ.get("PINN_BENCH_SHARED_GPU") == "1" and world > 1
-    gpu = 0 if shared else local_rank
-    torch.cuda.set_device(gpu)
-    dev = torch.device("cuda", gpu)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     group = None
     if world > 1:
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
-    # per-kernel CUDA events (FLAG_TIMING) only at N = 1, where they are graph
-    # nodes; the phased multi-GPU calls would synchronise the host per phase
-    tflag = FLAG_TIMING if world == 1 else 0
+    dp = None
     if args.method == "dp":
         # data-parallel vanilla PINN comparator: one 6x40 network on
         # [0,G]x[0,1] with C2's point count per GPU, points sharded, gradient all-reduce
         from paper_2104_10013_b200.binding import DataParallelPINN
+        from pinn_inputs import make_config
         prob = make_config("C2", method="pinn", weak=world, nx=1, ny=1,
                            n_f=16 * 15000 * world, n_u=960 * world)
-        dp = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=tflag)
-        h = dp.h
-        h_prob, local = h.prob, [0]
-    elif args.workload in ("c3", "c4", "c5"):
-        # C3 Burgers x-t XPINN 4x2 (8 x 20k residual points), C4 NS cavity XPINN 4x2
-        # (8 x 125k, the 1M-point strong-scaling case), C5 inverse heat (10-region map):
-        # fixed decompositions, subdomains placed on GPUs by LPT on their point counts
-        # (strong scaling)
-        prob = make_config(args.workload.upper(), method=args.method,
-                           **({"gpus": 8} if args.workload == "c3" else {}))
-        owner = lpt_owner([prob.n_points(q) for q in range(prob.n_sub)], world)
-        local = [q for q in range(prob.n_sub) if owner[q] == rank]
-        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | tflag)
-        h_prob = prob
+        scaling = "weak"
+        dp = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=0)
+        dpt = DataParallelPINN(prob, rank, world, device=dev, group=group, flags=FLAG_TIMING)
+        h, ht, local = dp.h, dpt.h, [0]
+        h_prob = dp.h.prob
     else:
-        prob = make_config("C2", method=args.method, weak=world)
-        owner = [s.ix // 4 for s in prob.subdomains]          # one 4x4 block per GPU
+        prob, owner, scaling = workload(args.workload, args.method, world)
         local = [q for q in range(prob.n_sub) if owner[q] == rank]
-        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | tflag)
+        # N > 1: the library's NCCL transport, the whole iteration (exchange
+        # included) one CUDA graph; N = 1: the fused single-GPU graph
+        xp = dict(transport="nccl", world=world, group=group) if world > 1 else {}
+        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH, **xp)
+        # a second handle with event-record nodes in its graph: per-kernel times
+        # (K1 roofline, compute / exchange split) in their own timed region, so
+        # the headline timing carries no event nodes
+        ht = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING, **xp)
         h_prob = prob
     stream = h.stream
     pts_local = h.n_points
 
-    def step():
-        if args.method == "dp":
-            dp.step(1)
-        elif world == 1:
-            h.step(1, want_loss=False)
+    def step(hh, dpp):
+        if dpp is not None:
+            dpp.step(1)
         else:
-            h.step_distributed(1, group)
+            hh.step(1, want_loss=False)
+
+    def timed_region(hh, dpp, n_steps, flush):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(n_steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(n_steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for k in range(n_steps):
+            flush.zero_()                                  # L2 flush, outside the events
+            starts[k].record(stream)
+            step(hh, dpp)
+            ends[k].record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        return [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
 
     for _ in range(args.warmup):
-        step()
+        step(h, dp)
     torch.cuda.synchronize(dev)
-    h.kernel_times()                                       # reset counters
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    clocks = ClockSampler(gpu)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.5)                                        # let nvidia-smi start sampling
-    for k in range(args.steps):
-        flush.zero_()                                      # L2 flush, outside the events
-        starts[k].record(stream)
-        step()
-        ends[k].record(stream)
-    torch.cuda.synchronize(dev)
+    step_ms = timed_region(h, dp, args.steps, flush)
     clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = sum(step_ms)
-    kt = h.kernel_times()                                  # K2, K1, K5 ms over the timed steps, launches
     t_local = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     pts_all = torch.tensor([pts_local], dtype=torch.float64, device=dev)
     res_loc = torch.tensor([float(sum(len(h_prob.subdomains[q].x_f) for q in local))], dtype=torch.float64,
@@ -341,159 +423,161 @@ def run_ours(args):
     value = float(pts_all.item()) * args.steps / (t_max * 1e-3)
     res_all = float(res_loc.item())
 
+    # ---- per-kernel breakdown: the same workload on the timing handle
+    dpt_ = dpt if dp is not None else None
+    for _ in range(args.warmup):
+        step(ht, dpt_)
+    ht.kernel_times()                                      # reset counters
+    n_t = max(3, min(args.steps, 100))
+    tstep_ms = timed_region(ht, dpt_, n_t, flush)
+    kt = ht.kernel_times()   # K2, K1, K5, launches, exchange, K1 interior, K1 interface, exposed wait (ms)
+    if dp is not None:
+        kt[1] = kt[1]                                      # loss_grad calls are phased: K1 accumulated per call
+
     # ---- end to end through the public API with host buffers (pinned H2D + D2H loss)
     host = [h.coords.cpu().pin_memory(), h.target.cpu().pin_memory(), h.mask.cpu().pin_memory()]
     h2d = sum(t.numel() * t.element_size() for t in host)
     d2h = h.n_sub * 8 * 4
     e2e_steps = max(3, min(args.steps, 50))
-    if world > 1:
-        dist.barrier()
-    pipelined = world == 1 and args.method != "dp"
-    if pipelined:
-        # a handle without FLAG_TIMING (whose per-step event read-back would
-        # synchronise the host every step); same problem, same initial state
-        he = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH)
-        for _ in range(args.warmup):
-            he.step(1, want_loss=False)
-        # N = 1: step k+1's inputs travel host -> device staging on a copy stream
-        # while step k computes; each step copies staging -> the point table
-        # (device), runs, and enqueues its loss read-back into pinned host memory
-        # (pinn_dd_read_loss); one synchronisation at the end
-        cs = torch.cuda.Stream(dev)
-        staging = [torch.empty_like(t, device=dev) for t in host]
-        loss_host = torch.empty(e2e_steps, he.n_sub, 8, dtype=torch.float32).pin_memory()
-        ev_in = [torch.cuda.Event() for _ in range(e2e_steps)]
-        ev_free = [torch.cuda.Event() for _ in range(e2e_steps)]
-        dst = [he.coords, he.target, he.mask]
-    def run_e2e(n):
-        for k in range(n):
-            if pipelined:
-                with torch.cuda.stream(cs):
-                    if k > 0:
-                        cs.wait_event(ev_free[k - 1])
-                    for sbuf, src in zip(staging, host):
-                        sbuf.copy_(src, non_blocking=True)
-                    ev_in[k].record(cs)
-                stream.wait_event(ev_in[k])
-                with torch.cuda.stream(stream):
-                    for d_, sbuf in zip(dst, staging):
-                        d_.copy_(sbuf, non_blocking=True)
-                    ev_free[k].record(stream)
-                he.step(1, want_loss=False)
-                he.read_loss(loss_host[k])                    # D2H of the loss breakdown (async)
-                continue
-            h.coords.copy_(host[0], non_blocking=True)
-            h.target.copy_(host[1], non_blocking=True)
-            h.mask.copy_(host[2], non_blocking=True)
-            if args.method == "dp":
-                dp.step(1, want_loss=True)
-            else:
-                h.step_distributed(1, group, want_loss=True)   # D2H of the loss breakdown
+    # step k+1's inputs travel host -> device staging on a copy stream while step
+    # k computes; each step copies staging -> the point table (device), runs,
+    # and enqueues its loss read-back into pinned host memory (pinn_dd_read_loss);
+    # one synchronisation at the end
+    cs = torch.cuda.Stream(dev)
+    staging = [torch.empty_like(t, device=dev) for t in host]
+    loss_host = torch.empty(e2e_steps + 3, h.n_sub, 8, dtype=torch.float32).pin_memory()
+    ev_in = [torch.cuda.Event() for _ in range(e2e_steps + 3)]
+    ev_free = [torch.cuda.Event() for _ in range(e2e_steps + 3)]
+    dst = [h.coords, h.target, h.mask]
 
-    run_e2e(3)                                             # untimed warm-up of the e2e loop
+    def run_e2e(k0, n):
+        for k in range(k0, k0 + n):
+            with torch.cuda.stream(cs):
+                if k > k0:
+                    cs.wait_event(ev_free[k - 1])
+                for sbuf, src in zip(staging, host):
+                    sbuf.copy_(src, non_blocking=True)
+                ev_in[k].record(cs)
+            stream.wait_event(ev_in[k])
+            with torch.cuda.stream(stream):
+                for d_, sbuf in zip(dst, staging):
+                    d_.copy_(sbuf, non_blocking=True)
+                ev_free[k].record(stream)
+            step(h, dp)
+            h.read_loss(loss_host[k])                      # D2H of the loss breakdown (async)
+
+    run_e2e(0, 3)                                          # untimed warm-up of the e2e loop
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    run_e2e(e2e_steps)
+    run_e2e(3, e2e_steps)
     torch.cuda.synchronize(dev)
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-    if pipelined:
-        if not bool(torch.isfinite(loss_host[:, :, 4]).all()):
-            raise SystemExit("non-finite loss in the e2e run")
-        he.close()
+    if not bool(torch.isfinite(loss_host[:, :, 4]).all()):
+        raise SystemExit("non-finite loss in the e2e run")
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_val = float(pts_all.item()) * e2e_steps / float(e2e_s.item())
 
     # ---- roofline of the dominant kernel (K1, fused loss + grad)
     k1_flops, k2_flops = algorithmic_flops(h_prob, local)
-    fused = world == 1 and args.method != "dp" and h.step_fused
+    fused = dp is None and ht.step_fused
     if fused:
         k1_flops += k2_flops          # the fused step runs K2's payload chunks inside K1
-    k1_ms = kt[1] / args.steps
-    k1_what = "K1 per launch (CUDA events inside the timed region)"
-    if world > 1:
-        # K1 (+ K5a) timed with events on the launching stream after the timed region
-        from paper_2104_10013_b200.binding import exchange_payload
-        ts = []
-        for _ in range(10):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            if args.method != "dp":
-                h.interface_payload()
-                exchange_payload(h.payload, h.table.plan, group)
-            e0.record(stream)
-            h.loss_grad(want_grad=False)
-            e1.record(stream)
-            ts.append((e0, e1))
-        torch.cuda.synchronize(dev)
-        k1_ms = sum(a.elapsed_time(b) for a, b in ts) / len(ts)
-        k1_what = "K1 + K5a per call, events on the launching stream after the timed region"
+    k1_ms = kt[1] / n_t
+    k1_what = ("K1 per step, event-record nodes inside the step graph of a timing handle, over its own "
+               f"timed region of {n_t} steps of the same workload")
     peak_fp32 = 148 * 128 * 2 * 1965e6 / 1e12              # TFLOP/s, FP32 FMA pipe at clocks.max.sm
     achieved = k1_flops / (k1_ms * 1e-3) / 1e12
+    # HBM side of the roofline (not the bound): algorithmic bytes per K1 launch
+    # and the ncu DRAM traffic, both per K1 time, vs the measured copy bandwidth
+    hbm_peak, hbm_src = 6547.8, "MEASURED_PEAKS.json hbm_gbs"
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        hbm_src = "MEASURED_PEAKS.json absent: this pool's measured 6547.8 GB/s"
+    alg_bytes = algorithmic_bytes(h_prob, local, h.n_fields)
     # DRAM bytes per K1 launch of THIS workload from one committed ncu --set full
     # capture (tools/dram_table.py); null when no capture of this workload exists
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_dram_bytes.json")
-    wl_key = f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}"
-    if os.path.exists(prof):
+    wl_key = f"{h_prob.name} {'data-parallel PINN' if dp is not None else h_prob.method}"
+    if os.path.exists(prof) and world == 1:
         try:
             ent = json.load(open(prof)).get(wl_key)
             traffic = ent.get("dram_bytes_per_launch") if ent else None
         except Exception:
             traffic = None
+    # compute / exchange split per step, max over ranks
+    split = torch.tensor([kt[0] / n_t, kt[1] / n_t, kt[2] / n_t, kt[4] / n_t, kt[7] / n_t], dtype=torch.float64,
+                         device=dev)
+    if world > 1:
+        dist.all_reduce(split, op=dist.ReduceOp.MAX)
+    split = split.tolist()
 
     if rank == 0:
         base = None
-        if world == 1 and not args.no_cpu and args.method != "dp":
-            base = cpu_baseline(make_config("C2", method=args.method) if args.workload == "c2" else
-                                make_config(args.workload.upper(), method=args.method,
-                                            **({"gpus": 8} if args.workload == "c3" else {})))
-        acts = sorted({prob.act(q) for q in local})
-        kname = (f"K1 k_fused<{prob.width},{prob.n_hidden},{prob.d_out},"
+        if world == 1 and not args.no_cpu and dp is None:
+            base = cpu_baseline(prob)
+        acts = sorted({h_prob.act(q) for q in local})
+        kname = (f"K1 k_fused<{h_prob.width},{h_prob.n_hidden},{h_prob.d_out},"
                  f"{'mixed' if len(acts) > 1 else acts[0]}> (fused fwd jets + loss + reverse"
                  f"{'; K2 interface payload in the same launch' if fused else ''})")
-        share = kt[1] / max(1e-9, sum(kt[:3])) if world == 1 else k1_ms / (t_max / args.steps)
+        share = k1_ms / (sum(tstep_ms) / n_t)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak" if args.workload == "c2" else "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            **({"shared_gpu_validation": "all ranks on cuda:0 over gloo: code-path check, not a bench number"}
-               if shared else {}),
             "iters_per_s": 1e3 * args.steps / t_max,
             "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
                         "p90": float(np.percentile(step_ms, 90))},
             "residual_points_per_s": res_all * args.steps / (t_max * 1e-3),   # N_F only (the paper's count)
-            "config": {"workload": f"{prob.name} {'data-parallel PINN' if args.method == 'dp' else prob.method}",
-                       "subdomains": prob.n_sub,
+            "config": {"workload": f"{h_prob.name} {'data-parallel PINN' if dp is not None else h_prob.method}",
+                       "subdomains": h_prob.n_sub,
                        "subdomains_per_gpu": len(local), "points_per_step": int(pts_all.item()),
-                       "net": f"2-{prob.width}x{prob.n_hidden}-{prob.d_out} {'/'.join(acts)}, adaptive slope n=10",
-                       "parallelism": f"domain decomposition, {len(local)} subdomains/GPU, P2P exchange",
+                       "net": f"2-{h_prob.width}x{h_prob.n_hidden}-{h_prob.d_out} {'/'.join(acts)}, "
+                              "adaptive slope n=10",
+                       "parallelism": (f"domain decomposition, {len(local)} subdomains/GPU, neighbour-only NCCL "
+                                       "send/recv inside the library's step graph" if world > 1 and dp is None else
+                                       f"domain decomposition, {len(local)} subdomains/GPU"
+                                       if dp is None else "data-parallel replicas, gradient all-reduce"),
                        "l2": "flushed (256 MiB write) between timed steps"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
                          "frac": achieved / peak_fp32, "traffic": traffic,
                          "kernel": kname,
                          "k1_ms_per_launch": k1_ms, "k1_timing": k1_what, "k1_gflop_per_launch": k1_flops / 1e9,
                          "k1_share_of_step": share,
-                         "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md clocks.max.sm)"},
-            "kernels_ms_per_step": {"K2_payload": (0.0 if fused else kt[0] / args.steps) if world == 1 else None,
-                                    "K2_inside_K1": fused,
-                                    "K1_loss_grad": k1_ms,
-                                    "K5_reduce_adam": kt[2] / args.steps if world == 1 else None},
-            "gpu_launches": int(kt[3]),
+                         "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md clocks.max.sm)",
+                         "hbm": {"algorithmic_bytes_per_launch": alg_bytes,
+                                 "algorithmic_gbs": alg_bytes / (k1_ms * 1e-3) / 1e9,
+                                 "traffic_gbs": (traffic / (k1_ms * 1e-3) / 1e9) if traffic else None,
+                                 "peak_gbs": hbm_peak, "peak_source": hbm_src,
+                                 "frac": (traffic if traffic else alg_bytes) / (k1_ms * 1e-3) / 1e9 / hbm_peak,
+                                 "frac_of": "ncu DRAM traffic" if traffic else "algorithmic bytes"}},
+            "kernels_ms_per_step": {"K2_payload": split[0], "K2_inside_K1": fused, "K1_loss_grad": split[1],
+                                    "K5_reduce_adam": split[2], "exchange": split[3],
+                                    "exchange_exposed": split[4], "timing_steps": n_t,
+                                    "how": "event-record nodes in the step graph of the timing handle; max over "
+                                           "ranks; exchange = NCCL group on the exchange stream from the end of "
+                                           "K2, exposed = wait of the compute stream after K1 interior"},
+            "gpu_launches": int(kt[3] * args.steps / n_t),
             "clocks": clk,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "how": ("pinned H2D of step k+1's point table on a copy stream overlapping step k, "
-                            "device copy into the table, pinn_dd_step, async D2H of the loss breakdown; "
-                            "one sync at the end; wall clock" if pipelined else
-                            "pinned H2D of the point table, step, synchronous D2H of the loss; wall clock"),
+                            "device copy into the table, the step, async D2H of the loss breakdown "
+                            "(pinn_dd_read_loss); one sync at the end; wall clock, max over ranks"),
                     "steps": e2e_steps},
             "cpu_baseline": base,
         }
         print(json.dumps(line))
-    h.close()
+    if dp is not None:
+        dp.close()
+        dpt.close()
+    else:
+        h.close()
+        ht.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -509,9 +593,10 @@ def main():
                     help="default cpinn for c2, xpinn for c5; dp = data-parallel vanilla PINN comparator "
                          "(Table 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c2",
-                    help="c2: BASELINE configs[1] (default, the headline); c3/c4/c5: configs[2..4] "
-                         "(fixed decompositions, strong scaling)")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c4",
+                    help="c4: BASELINE configs[3] (default: the largest single-GPU config, strong); "
+                         "c2: configs[1] (strong, 16/N subdomains per GPU); c3: configs[2] (weak, one "
+                         "subdomain per GPU); c5: configs[4] (LPT placement, strong)")
     args = ap.parse_args()
     if args.method is None:
         args.method = "cpinn" if args.workload == "c2" else "xpinn"

@@ -60,9 +60,9 @@ typedef enum {
   PINN_DD_EINVAL = 1,        /* shape / count / pointer mismatch, cPINN with a time-axis interface */
   PINN_DD_EUNSUPPORTED = 2,  /* (width, n_hidden, d_out, activation) not compiled in */
   PINN_DD_ECUDA = 3,         /* CUDA runtime error; message carries cudaGetErrorString */
-  PINN_DD_ENCCL = 4,         /* reserved */
+  PINN_DD_ENCCL = 4,         /* NCCL unavailable or an NCCL call failed (message carries NCCL's text) */
   PINN_DD_ENONFINITE = 5,    /* a loss J_q or gradient is NaN/Inf (message names the subdomain) */
-  PINN_DD_EPROTOCOL = 6      /* interface segment without a twin, remote twin used by pinn_dd_step */
+  PINN_DD_EPROTOCOL = 6      /* malformed twin / exchange plan; remote twins without a transport */
 } pinn_dd_status;
 
 /* HYBRID ("cPINN in space + XPINN in time"): per interface edge, normal-flux
@@ -75,13 +75,25 @@ enum { PINN_DD_METHOD_PINN = 0, PINN_DD_METHOD_CPINN = 1, PINN_DD_METHOD_XPINN =
 enum { PINN_DD_PDE_BURGERS = 0, PINN_DD_PDE_POISSON = 1, PINN_DD_PDE_HEAT = 2, PINN_DD_PDE_NS = 3,
        PINN_DD_PDE_HEAT_INV = 4 };
 enum { PINN_DD_ACT_TANH = 0, PINN_DD_ACT_SIN = 1, PINN_DD_ACT_COS = 2 };
+/* Eq. (4) geometry of the decomposition: which subdomains own a point. */
+enum { PINN_DD_GEOM_NONE = 0,     /* no geometry: only pinn_dd_predict_owners            */
+       PINN_DD_GEOM_BOXES = 1,    /* Cartesian cells [lo_x, hi_x] x [lo_y, hi_y] (closed)   */
+       PINN_DD_GEOM_VORONOI = 2   /* nearest-seed cells clipped by a simple polygon (C5)    */ };
+/* pinn_dd_predict modes */
+enum { PINN_DD_PREDICT_STITCHED = 0,  /* Eq. (4): average of the owners' nets, weight 1/S       */
+       PINN_DD_PREDICT_OWNER = 1 };   /* the net of the lowest-id owner only (weight 1)         */
 
 /* flags */
 #define PINN_DD_FLAG_GRAPH        1  /* pinn_dd_step replays a captured CUDA graph */
 #define PINN_DD_FLAG_GLOBAL_STASH 2  /* keep the reverse-mode stash in global memory instead of TMEM (debug) */
 #define PINN_DD_FLAG_TIMING       4  /* record per-kernel CUDA events (see pinn_dd_kernel_times) */
-#define PINN_DD_FLAG_POINT_PER_THREAD 8 /* width-20 nets: one thread per point (all neurons in
-                                           registers) instead of the default neuron-block kernel */
+
+/* Status bits of one loss + gradient evaluation (loss column 5, per subdomain).
+   A slope a^k that reaches 0 (set_params, or Adam) makes its gradient NaN. */
+#define PINN_DD_STATUS_J_NONFINITE      1
+#define PINN_DD_STATUS_GRAD_NONFINITE   2
+#define PINN_DD_STATUS_SLOPE_NONFINITE  4
+#define PINN_DD_STATUS_SLOPE_ZERO       8
 
 /* Per-subdomain hyper-parameters, P:151-161 (loss weights) and P:286 (Adam). */
 typedef struct {
@@ -125,7 +137,10 @@ typedef struct {
   const float* coords;       /* [2][n_points]                                      */
   const float* target;       /* [d_out][n_points]   training targets u^(i)         */
   const float* mask;         /* [d_out][n_points]   1 = constrained output         */
-  const float* init_params;  /* [n_sub][pinn_dd_n_params(...)] packed, or NULL = 0 */
+  const float* init_params;  /* [n_sub][pinn_dd_n_params(...)] packed, or NULL = W = b = 0,
+                                a^k = 1/slope_n.  Every a^k must be finite and non-zero
+                                (EINVAL): the slope gradient uses a^k dJ/da^k = <W^k, dJ/dW^k> +
+                                <b^k, dJ/db^k>, undefined at a^k = 0         */
   /* ---- runtime --------------------------------------------------------- */
   void* stream;              /* cudaStream_t (NULL = legacy default stream)        */
   int32_t flags;             /* PINN_DD_FLAG_*                                     */
@@ -139,6 +154,38 @@ typedef struct {
                                 P:862-866: tanh / sin / cos per region); NULL = `activation`
                                 everywhere.  Mixed values need a network shape compiled with
                                 per-subdomain activations (else PINN_DD_EUNSUPPORTED). */
+  /* ---- exchange with other ranks (Algorithm 1 green stage; host, copied) ---
+     Rows [n_points, n_points + n_recv) of the payload buffer are received from
+     other ranks.  With an NCCL transport (nccl_id != NULL) pinn_dd_step runs the
+     whole iteration itself -- K2, ncclSend/ncclRecv of the cut-edge rows on an
+     internal stream overlapped with K1 over the residual + training points, K1
+     over the interface points, K5 -- captured into one CUDA graph.  A peer may be
+     this rank itself (loop-back; single-GPU validation of the transport).      */
+  int32_t rank;              /* rank of this process in the exchange communicator          */
+  int32_t world;             /* communicator size (ignored when nccl_id == NULL)            */
+  int32_t n_peers;           /* ranks this handle exchanges rows with                       */
+  const int32_t* peer_rank;  /* [n_peers] distinct, ascending                               */
+  const int64_t* peer_send_off; /* [n_peers + 1] offsets into send_rows                     */
+  const int64_t* send_rows;  /* local interface-point rows (< n_points) sent to each peer, in
+                                the order that peer receives them                           */
+  const int64_t* peer_recv_row; /* [n_peers] first received row; ranges tile
+                                [n_points, n_points + n_recv) in peer order                 */
+  const int64_t* peer_recv_n;   /* [n_peers] rows received from each peer                  */
+  const void* nccl_id;       /* 128-byte ncclUniqueId (host) shared by the `world` ranks
+                                (pinn_dd_nccl_unique_id on one rank, broadcast by the caller);
+                                pinn_dd_create then joins the communicator (collective: every
+                                rank must call it).  NULL = no transport: the caller moves
+                                received rows itself between the phased calls.              */
+  /* ---- Eq. (4) geometry (host, copied; optional) -------------------------- */
+  int32_t geometry;          /* PINN_DD_GEOM_*                                               */
+  int32_t n_geo;             /* subdomains of the WHOLE decomposition described below       */
+  const float* geo;          /* BOXES: [n_geo][4] (lo_x, lo_y, hi_x, hi_y); VORONOI: [n_geo][2] seeds */
+  const int32_t* geo_local;  /* [n_geo] local subdomain index of each entry, -1 = owned by another rank */
+  int32_t n_poly;            /* VORONOI: vertices of the simple domain polygon             */
+  const float* poly;         /* [n_poly][2]                                                   */
+  float geo_tol;             /* BOXES: a point within geo_tol of a cell is in it (closed cells);
+                                VORONOI: seeds whose squared distance is within geo_tol of the
+                                nearest one are co-owners (points on interfaces, weight 1/S) */
 } pinn_dd_desc;
 
 /* Number of packed parameters of one network [d_in, width x n_hidden, d_out]:
@@ -169,7 +216,8 @@ pinn_dd_status pinn_dd_payload_buffer(pinn_dd* h, float** buf, int32_t* n_fields
    interface) and g_q = dJ_q/dTheta_q with every neighbour value
    constant, for all local q.  Requires a current payload buffer.
    loss_dev (nullable): device [n_sub][8] = {MSE_u, MSE_F, MSE_uavg,
-   MSE_flux|MSE_R, J, 0, 0, 0}.  grad_dev (nullable): device [n_sub][n_params]
+   MSE_flux|MSE_R, J, status, 0, 0}; status = OR of PINN_DD_STATUS_* bits of
+   this evaluation (0 = all finite).  grad_dev (nullable): device [n_sub][n_params]
    packed gradient. */
 pinn_dd_status pinn_dd_loss_grad(pinn_dd* h, float* loss_dev, float* grad_dev);
 
@@ -188,28 +236,51 @@ pinn_dd_status pinn_dd_loss_grad_interface(pinn_dd* h, float* loss_dev, float* g
    on every local subdomain with the gradient of the last pinn_dd_loss_grad. */
 pinn_dd_status pinn_dd_adam(pinn_dd* h);
 
-/* n_iters x (payload -> loss+grad -> Adam), one synchronous Jacobi iteration
-   each (payloads from the parameters at the start of the iteration).  Only for
-   handles with n_recv == 0 (else PINN_DD_EPROTOCOL).  With PINN_DD_FLAG_GRAPH
-   the three launches are captured once and replayed.  loss_host (nullable):
-   host [n_sub][8] breakdown of the LAST iteration (synchronises); a non-finite
-   J returns PINN_DD_ENONFINITE. */
+/* n_iters x (payload -> [exchange] -> loss+grad -> Adam), one synchronous
+   Jacobi iteration each (payloads from the parameters at the start of the
+   iteration, Algorithm 1).  Handles with remote twins (n_recv > 0)
+   need the NCCL transport (desc nccl_id; else PINN_DD_EPROTOCOL); every rank
+   must call pinn_dd_step with the same n_iters.  With PINN_DD_FLAG_GRAPH the
+   iteration is captured once into a CUDA graph (exchange included) and
+   replayed.  loss_host (nullable):
+   host [n_sub][8] breakdown of the LAST iteration (synchronises); a non-zero
+   status column (non-finite J or gradient, zero slope) returns
+   PINN_DD_ENONFINITE naming the subdomain. */
 pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host);
 
+/* The library's exchange (NCCL transport only) as a stream-ordered call for the
+   phased path: sends the cut-edge rows written by the last
+   pinn_dd_interface_payload and receives rows [n_points, n_points + n_recv)
+   (ncclGroupStart / ncclSend / ncclRecv / ncclGroupEnd on desc->stream).
+   Collective over the peers: they must all call it. */
+pinn_dd_status pinn_dd_exchange(pinn_dd* h);
+
+/* A fresh 128-byte ncclUniqueId (host) for desc->nccl_id (PINN_DD_ENCCL if NCCL
+   cannot be loaded). */
+pinn_dd_status pinn_dd_nccl_unique_id(void* id128);
+
 /* Stream-ordered copy of the loss breakdown [n_sub][8] (MSE_u, MSE_F,
-   MSE_uavg, MSE_if, J_q (Eq. 5/6), non-finite flag, 0, 0) of the last
+   MSE_uavg, MSE_if, J_q (Eq. 5/6), status bits, 0, 0) of the last
    loss+grad evaluation into dst (pinned host or device memory, caller-owned).
-   No synchronisation and no non-finite check (read the flag column, or call
+   No synchronisation and no status check (read the status column, or call
    pinn_dd_step with loss_host); lets a caller pipeline the per-step loss
    read-back with the next step. */
 pinn_dd_status pinn_dd_read_loss(pinn_dd* h, float* dst);
 
-/* K6: Eq. (4) stitched solution u(z) = sum_q u_q(z) 1_{Omega_q}(z) with weight
-   1/S at points shared by S subdomains.  pts: device [2][n]; owners: device
-   [n][4] local subdomain ids (-1 = unused), the caller's point classification;
-   out: device [d_out][n]. */
-pinn_dd_status pinn_dd_predict(pinn_dd* h, const float* pts, const int32_t* owners, int64_t n,
-                               float* out);
+/* K6: Eq. (4) stitched solution u(z) = sum_q u_q(z) 1_{Omega_q}(z)
+   with the indicator 1 inside Omega_q, 1/S on an interface shared by S
+   subdomains and 0 outside every subdomain; the owners of each point are
+   classified by the library from desc->geometry (EINVAL without one).  pts:
+   device [2][n]; out: device [d_out][n].  mode PINN_DD_PREDICT_STITCHED
+   (Eq. 4) or PINN_DD_PREDICT_OWNER (the lowest-id owner's net, weight 1).  S
+   counts owners on every rank; a handle adds only its LOCAL owners' terms, so
+   with several ranks the caller sums `out` over ranks (e.g. an all-reduce). */
+pinn_dd_status pinn_dd_predict(pinn_dd* h, const float* pts, int64_t n, float* out, int32_t mode);
+
+/* Same as pinn_dd_predict(STITCHED) with the caller's classification: owners
+   device [n][4] local subdomain ids (-1 = unused), weight 1/(number of ids). */
+pinn_dd_status pinn_dd_predict_owners(pinn_dd* h, const float* pts, const int32_t* owners, int64_t n,
+                                      float* out);
 
 /* Parameter / optimiser state access (device buffers of n_params floats,
    packed layout).  what: 0 = Theta, 1 = Adam m, 2 = Adam v, 3 = last gradient. */
@@ -218,11 +289,14 @@ pinn_dd_status pinn_dd_set_params(pinn_dd* h, int32_t sub, int32_t what, const f
 /* Adam step counter t of subdomain `sub` (host; synchronises). */
 pinn_dd_status pinn_dd_get_step(pinn_dd* h, int32_t sub, int32_t* t);
 
-/* With PINN_DD_FLAG_TIMING: cumulative device milliseconds of
-   {K2 payload, K1 loss+grad, K5 reduce/adam, launches counted} since the last
-   call (synchronises, then resets).  When pinn_dd_step runs fused (below) K2's
-   work is inside K1 and its entry is 0. */
-pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4);
+/* With PINN_DD_FLAG_TIMING: cumulative device milliseconds since the last call
+   (synchronises, then resets) of ms8 = {K2 payload, K1 loss+grad, K5
+   reduce/adam, launches counted, exchange (NCCL group on the exchange stream,
+   from the end of K2), K1 interior part, K1 interface part, exposed exchange
+   (time the step's stream waited for the exchange after K1 interior)}.  When
+   pinn_dd_step runs fused (below) K2's work is inside K1 and its entry is 0;
+   entries 4-7 are 0 without remote twins. */
+pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms8);
 
 /* 1 if pinn_dd_step runs the interface payload (K2) and the loss + gradient
    (K1) as one persistent launch: payload chunks first, interface loss chunks

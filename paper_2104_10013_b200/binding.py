@@ -25,12 +25,16 @@ OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, ENONFINITE, EPROTOCOL = range(7)
 METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2, "hybrid": 3}
 PDES = {"burgers": 0, "poisson": 1, "heat": 2, "ns": 3, "heat_inv": 4}
 ACTS = {"tanh": 0, "sin": 1, "cos": 2}
-FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING, FLAG_POINT_PER_THREAD = 1, 2, 4, 8
+FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING = 1, 2, 4
+GEOM_NONE, GEOM_BOXES, GEOM_VORONOI = 0, 1, 2
+PREDICT_STITCHED, PREDICT_OWNER = 0, 1
+STATUS_J, STATUS_GRAD, STATUS_SLOPE, STATUS_SLOPE_ZERO = 1, 2, 4, 8
 
 EXPORTS = [
     "pinn_dd_n_params", "pinn_dd_workspace_size", "pinn_dd_create", "pinn_dd_interface_payload",
     "pinn_dd_payload_buffer", "pinn_dd_loss_grad", "pinn_dd_loss_grad_interior", "pinn_dd_loss_grad_interface",
-    "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict",
+    "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict", "pinn_dd_predict_owners", "pinn_dd_exchange",
+    "pinn_dd_nccl_unique_id",
     "pinn_dd_get_params", "pinn_dd_set_params", "pinn_dd_get_step", "pinn_dd_kernel_times",
     "pinn_dd_plan_info", "pinn_dd_step_fused", "pinn_dd_read_loss", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
 ]
@@ -64,6 +68,13 @@ class Desc(C.Structure):
         ("stream", C.c_void_p), ("flags", C.c_int32),
         ("sub_norm_counts", C.POINTER(C.c_int32)),
         ("sub_activation", C.POINTER(C.c_int32)),
+        ("rank", C.c_int32), ("world", C.c_int32), ("n_peers", C.c_int32),
+        ("peer_rank", C.POINTER(C.c_int32)), ("peer_send_off", C.POINTER(C.c_int64)),
+        ("send_rows", C.POINTER(C.c_int64)), ("peer_recv_row", C.POINTER(C.c_int64)),
+        ("peer_recv_n", C.POINTER(C.c_int64)), ("nccl_id", C.c_void_p),
+        ("geometry", C.c_int32), ("n_geo", C.c_int32), ("geo", C.POINTER(C.c_float)),
+        ("geo_local", C.POINTER(C.c_int32)), ("n_poly", C.c_int32), ("poly", C.POINTER(C.c_float)),
+        ("geo_tol", C.c_float),
     ]
 
 
@@ -90,7 +101,10 @@ def load_library(path: str = LIB_PATH):
     lib.pinn_dd_loss_grad_interface.argtypes = [vp, vp, vp]
     lib.pinn_dd_adam.argtypes = [vp]
     lib.pinn_dd_step.argtypes = [vp, i32, f32p]
-    lib.pinn_dd_predict.argtypes = [vp, vp, vp, i64, vp]
+    lib.pinn_dd_predict.argtypes = [vp, vp, i64, vp, i32]
+    lib.pinn_dd_predict_owners.argtypes = [vp, vp, vp, i64, vp]
+    lib.pinn_dd_exchange.argtypes = [vp]
+    lib.pinn_dd_nccl_unique_id.argtypes = [vp]
     lib.pinn_dd_get_params.argtypes = [vp, i32, i32, vp]
     lib.pinn_dd_set_params.argtypes = [vp, i32, i32, vp]
     lib.pinn_dd_get_step.argtypes = [vp, i32, C.POINTER(i32)]
@@ -147,12 +161,18 @@ class PointTable:
 
 
 def build_point_table(prob, local: Sequence[int], owner: Optional[Sequence[int]] = None,
-                      rank: int = 0) -> PointTable:
+                      rank: int = 0, peer_of=None) -> PointTable:
     """Lay out the point sets of the `local` subdomains (global ids) in the
-    order the ABI expects; twins of edges whose neighbour lives on another rank
-    (owner[nb] != rank) get receive rows after the local points."""
+    order the ABI expects.  An edge is cut when its two subdomains have
+    different owners; the twin of a cut edge's segment is a receive row after
+    the local points, filled by the exchange with rank peer_of(owner[nb])
+    (identity by default; a loop-back plan maps every owner to this rank, so a
+    single process exchanges with itself).  Per peer, rows are sent in (edge,
+    sender) order and received in (edge, neighbour) order, so both sides of
+    every cut edge agree on the order."""
     local = list(local)
     owner = list(owner) if owner is not None else [rank] * prob.n_sub
+    peer_of = peer_of or (lambda o: o)
     d_out = prob.d_out
     xs, ts, ms = [], [], []
     sub_off, n_res, n_data, seg_off = [0], [], [], [0]
@@ -180,9 +200,10 @@ def build_point_table(prob, local: Sequence[int], owner: Optional[Sequence[int]]
     recv_edges: Dict[int, List[Tuple[int, int, int]]] = {}
     for q, e, st, n in zip(seg_sub, seg_edge, seg_start, seg_n):
         nb = prob.edge_neighbor(q, e)
-        if owner[nb] != rank:
-            send.setdefault(owner[nb], []).append((e, q, st, n))
-            recv_edges.setdefault(owner[nb], []).append((e, q, st, n))
+        if owner[nb] != owner[q]:
+            peer = peer_of(owner[nb])
+            send.setdefault(peer, []).append((e, q, st, n))
+            recv_edges.setdefault(peer, []).append((e, nb, q, n))
     seg_twin = np.zeros(len(seg_n), dtype=np.int64)
     recv_rows: Dict[int, Tuple[int, int]] = {}
     row = n_points
@@ -190,13 +211,13 @@ def build_point_table(prob, local: Sequence[int], owner: Optional[Sequence[int]]
     for peer in sorted(recv_edges):
         lst = sorted(recv_edges[peer])
         start = row
-        for e, q, st, n in lst:
+        for e, nb, q, n in lst:
             remote_slot[(q, e)] = row
             row += n
         recv_rows[peer] = (start, row - start)
     for i, (q, e, st) in enumerate(zip(seg_sub, seg_edge, seg_start)):
         nb = prob.edge_neighbor(q, e)
-        seg_twin[i] = where[(nb, e)] if owner[nb] == rank else remote_slot[(q, e)]
+        seg_twin[i] = where[(nb, e)] if owner[nb] == owner[q] else remote_slot[(q, e)]
     send_idx = {}
     for peer, lst in send.items():
         idx = [np.arange(st, st + n) for e, q, st, n in sorted(lst)]
@@ -250,22 +271,75 @@ def make_desc(prob, t: PointTable, dev_ptrs: Dict[str, int], stream: int = 0, fl
     acts = [ACTS[prob.act(q)] for q in t.local]
     if any(a != d.activation for a in acts):
         d.sub_activation = ptr(np.asarray(acts, dtype=np.int32), C.c_int32)
+    # exchange plan (peers ascending; received ranges in the same order)
+    peers = sorted(set(t.plan.send) | set(t.plan.recv))
+    if peers:
+        sends = [np.asarray(t.plan.send.get(p, np.zeros(0, np.int64)), np.int64) for p in peers]
+        off = np.concatenate([[0], np.cumsum([len(x) for x in sends])]).astype(np.int64)
+        d.n_peers = len(peers)
+        d.peer_rank = ptr(np.asarray(peers, np.int32), C.c_int32)
+        d.peer_send_off = ptr(off, C.c_int64)
+        d.send_rows = ptr(np.concatenate(sends) if off[-1] else np.zeros(1, np.int64), C.c_int64)
+        row = int(t.coords.shape[1])
+        rr, rn = [], []
+        for p in peers:
+            r0, n = t.plan.recv.get(p, (row, 0))
+            rr.append(r0)
+            rn.append(n)
+            row = r0 + n
+        d.peer_recv_row = ptr(np.asarray(rr, np.int64), C.c_int64)
+        d.peer_recv_n = ptr(np.asarray(rn, np.int64), C.c_int64)
+    # Eq. (4) geometry of the whole decomposition
+    pos = {q: i for i, q in enumerate(t.local)}
+    d.geo_local = ptr(np.asarray([pos.get(q, -1) for q in range(prob.n_sub)], np.int32), C.c_int32)
+    d.n_geo = prob.n_sub
+    if "seeds" in prob.meta:
+        d.geometry = GEOM_VORONOI
+        d.geo = ptr(np.asarray(prob.meta["seeds"], np.float32).reshape(-1), C.c_float)
+        poly = np.asarray(prob.meta["polygon"], np.float32)
+        d.n_poly = len(poly)
+        d.poly = ptr(poly.reshape(-1), C.c_float)
+        d.geo_tol = 1e-5
+    else:
+        d.geometry = GEOM_BOXES
+        d.geo = ptr(np.asarray([[s.lo[0], s.lo[1], s.hi[0], s.hi[1]] for s in prob.subdomains],
+                               np.float32).reshape(-1), C.c_float)
+        d.geo_tol = 0.0
     return d, keep
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId from the library's NCCL (pinn_dd_nccl_unique_id)."""
+    lib = load_library()
+    buf = (C.c_char * 128)()
+    st = lib.pinn_dd_nccl_unique_id(buf)
+    if st != OK:
+        raise PinnDDError(st, lib.pinn_dd_last_error(None).decode())
+    return bytes(buf)
+
+
 class PinnDD:
-    """One handle per GPU: the subdomains `local` of `prob`."""
+    """One handle per GPU: the subdomains `local` of `prob`.
+
+    transport="nccl": cut-edge payload rows move inside the library (NCCL P2P
+    on an internal stream, captured with the rest of the iteration into one
+    CUDA graph by pinn_dd_step).  With world > 1, rank 0 draws the NCCL id and
+    `group` (a torch.distributed process group, any backend) broadcasts it.
+    loopback=True (single process): edges between different owners are
+    exchanged with this rank itself through NCCL -- the multi-GPU data path
+    validated on one GPU."""
 
     def __init__(self, prob, local: Optional[Sequence[int]] = None, owner: Optional[Sequence[int]] = None,
                  rank: int = 0, device=None, flags: int = FLAG_GRAPH, hparams: Optional[Sequence] = None,
-                 norm_counts: Optional[Sequence] = None):
+                 norm_counts: Optional[Sequence] = None, transport: Optional[str] = None, world: int = 1,
+                 group=None, loopback: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("PinnDD needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
         self.prob = prob
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         local = list(range(prob.n_sub)) if local is None else list(local)
-        self.table = build_point_table(prob, local, owner, rank)
+        self.table = build_point_table(prob, local, owner, rank, peer_of=(lambda o: rank) if loopback else None)
         t = self.table
         dev = self.device
         self.n_sub = len(local)
@@ -281,6 +355,21 @@ class PinnDD:
         d, self._keep = make_desc(prob, t, dict(coords=self.coords.data_ptr(), target=self.target.data_ptr(),
                                                mask=self.mask.data_ptr(), init_params=self.init_params.data_ptr()),
                                   self.stream.cuda_stream, flags, hparams, norm_counts)
+        nccl_id = None
+        if transport == "nccl":
+            if world > 1:
+                import torch.distributed as dist
+                obj = [nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                nccl_id = obj[0]
+            else:
+                nccl_id = nccl_unique_id()
+            self._nccl_id = C.create_string_buffer(nccl_id, 128)
+            d.nccl_id = C.cast(self._nccl_id, C.c_void_p)
+            d.rank, d.world = (0, 1) if loopback else (rank, world)
+        elif transport is not None:
+            raise ValueError(f"unknown transport {transport!r}")
+        self.transport = transport
         self.desc = d
         nbytes = C.c_size_t(0)
         self._check(self.lib.pinn_dd_workspace_size(C.byref(d), C.byref(nbytes)), None)
@@ -367,14 +456,27 @@ class PinnDD:
             self.adam()
         return self._loss_dev.cpu().numpy() if want_loss else None
 
-    def predict(self, pts: torch.Tensor, owners: torch.Tensor) -> torch.Tensor:
-        """pts [2, n] float32, owners [n, 4] int32 local ids (-1 unused) -> [d_out, n]."""
+    def predict(self, pts: torch.Tensor, owners: Optional[torch.Tensor] = None, mode: str = "stitched") -> torch.Tensor:
+        """Eq. (4): pts [2, n] float32 -> [d_out, n].  Owners classified by the
+        library from the decomposition's geometry (mode "stitched": 1/S
+        average; "owner": lowest-id owner), or the caller's owners [n, 4] int32
+        local ids (-1 unused).  With several ranks each returns its local
+        owners' share (sum over ranks)."""
         n = pts.shape[1]
         out = torch.empty(self.prob.d_out, n, dtype=torch.float32, device=self.device)
-        pts = pts.contiguous(); owners = owners.contiguous()
-        self._check(self.lib.pinn_dd_predict(self.h, C.c_void_p(pts.data_ptr()), C.c_void_p(owners.data_ptr()),
-                                             n, C.c_void_p(out.data_ptr())))
+        pts = pts.contiguous()
+        if owners is not None:
+            owners = owners.contiguous()
+            self._check(self.lib.pinn_dd_predict_owners(self.h, C.c_void_p(pts.data_ptr()),
+                                                        C.c_void_p(owners.data_ptr()), n, C.c_void_p(out.data_ptr())))
+        else:
+            m = {"stitched": PREDICT_STITCHED, "owner": PREDICT_OWNER}[mode]
+            self._check(self.lib.pinn_dd_predict(self.h, C.c_void_p(pts.data_ptr()), n, C.c_void_p(out.data_ptr()), m))
         return out
+
+    def exchange(self):
+        """The library's NCCL exchange of the cut-edge payload rows (phased path)."""
+        self._check(self.lib.pinn_dd_exchange(self.h))
 
     def get(self, q: int, what: int = 0) -> torch.Tensor:
         out = torch.empty(self.n_params, dtype=torch.float32, device=self.device)
@@ -402,7 +504,8 @@ class PinnDD:
         return bool(self.lib.pinn_dd_step_fused(self.h))
 
     def kernel_times(self):
-        ms = (C.c_double * 4)()
+        """[K2, K1, K5, launches, exchange, K1 interior, K1 interface, exposed exchange wait] (ms)."""
+        ms = (C.c_double * 8)()
         self._check(self.lib.pinn_dd_kernel_times(self.h, ms))
         return list(ms)
 

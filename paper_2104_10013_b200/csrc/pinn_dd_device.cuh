@@ -497,6 +497,8 @@ struct KArgs {
   float* partial;           // [n_chunks][pstride]
   float* partial_loss;      // [n_chunks][4]
   float* payload;           // [rows][NF]
+  const int32_t* psend;     // [n_points] row of the point in the send buffer, -1 = not sent (nullptr: no peers)
+  float* sendbuf;           // [n_send][NF] payload rows of cut edges, in the peers' receive order
   float* gstash;            // global stash fallback (nullptr = TMEM)
   PdeConst pc;
   int method;               // 0 pinn, 1 cpinn, 2 xpinn, 3 hybrid (per-edge choice in pinfo bit 2)

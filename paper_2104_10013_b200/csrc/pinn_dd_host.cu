@@ -7,6 +7,7 @@
 // K2 (payload) -> K1 (loss + grad) -> K5 (reduce + Adam) on the caller's stream,
 // optionally captured once into a CUDA graph.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -19,7 +20,6 @@
 
 #include "../../include/pinn_dd.h"
 #include "pinn_dd_kernels.cuh"
-#include "pinn_dd_kernels_pt.cuh"
 
 using namespace pinn;
 
@@ -28,11 +28,65 @@ namespace {
 thread_local std::string g_create_error;
 
 // -------------------------------------------------------------------------
+// NCCL, resolved at run time (dlopen of libnccl.so.2: the copy the process
+// already loaded -- PyTorch's -- is reused, so one NCCL serves both).  Only
+// the stable C API below is used (types as in nccl.h).
+// -------------------------------------------------------------------------
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;            // ncclSuccess = 0
+constexpr int kNcclFloat32 = 7;      // ncclFloat32
+struct Nccl {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const Nccl& nccl() {
+  static const Nccl n = [] {
+    Nccl r;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+      const char* e = dlerror();
+      r.why = std::string("dlopen(libnccl.so.2): ") + (e ? e : "not found");
+      return r;
+    }
+    bool all = true;
+    auto get = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(lib, name));
+      if (!fn) {
+        all = false;
+        r.why = std::string("libnccl.so.2 lacks ") + name;
+      }
+    };
+    get(r.GetUniqueId, "ncclGetUniqueId");
+    get(r.CommInitRank, "ncclCommInitRank");
+    get(r.CommDestroy, "ncclCommDestroy");
+    get(r.CommAbort, "ncclCommAbort");
+    get(r.Send, "ncclSend");
+    get(r.Recv, "ncclRecv");
+    get(r.GroupStart, "ncclGroupStart");
+    get(r.GroupEnd, "ncclGroupEnd");
+    get(r.GetErrorString, "ncclGetErrorString");
+    r.ok = all;
+    return r;
+  }();
+  return n;
+}
+
+// -------------------------------------------------------------------------
 // compiled network shapes
 // -------------------------------------------------------------------------
 struct Ops {
   int N, NH, DO, ACT;
-  int pt;          // 1: point-per-thread kernel (narrow nets), 0: neuron-block kernel
   int pstride;     // Lay::total()
   int P;           // points per tile
   int threads;     // threads per CTA of the fused kernels
@@ -41,46 +95,36 @@ struct Ops {
   void (*k1)(const KArgs&, int grid, size_t smem, cudaStream_t);
   void (*k2)(const KArgs&, int grid, size_t smem, cudaStream_t);
   void (*kf)(const KArgs&, int grid, size_t smem, cudaStream_t);   // fused payload + loss/grad (nullptr: none)
-  void (*pred)(const float*, int, float, const float*, const int32_t*, int64_t, float*, const int32_t*,
-               cudaStream_t);
+  void (*pred)(const float*, int, float, const float*, const Geo&, int64_t, float*, const int32_t*, cudaStream_t);
   void (*packmap)(std::vector<int32_t>&);
   void (*slopetab)(RArgs&);
   cudaError_t (*setattr)(size_t);
 };
 
-template <int N, int NH, int DO, int ACT, bool PT = false, int T = kThreads>
+template <int N, int NH, int DO, int ACT, int T = kThreads>
 struct Inst {
   using C = KCfg<N, NH, DO, T>;
   using LY = Lay<N, NH, DO>;
   static size_t smem() {   // >= 120 KB forces 1 CTA / SM (the CTA owns all of TMEM)
-    if constexpr (PT)
-      return std::max<size_t>(PtCfg<N, NH, DO>::SMEM, 120 * 1024);
-    else if constexpr (T == 256)
+    if constexpr (T == 256)
       return std::max<size_t>(C::SMEM, 120 * 1024);
     else
       return C::SMEM;   // two 128-thread CTAs per SM, 256 TMEM columns each
   }
   static void k1(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
-    if constexpr (PT)
-      k_fused_pt<N, NH, DO, ACT, 0><<<grid, kPT, sm, s>>>(a);
-    else
-      k_fused<N, NH, DO, ACT, 0, T><<<grid, T, sm, s>>>(a);
+    k_fused<N, NH, DO, ACT, 0, T><<<grid, T, sm, s>>>(a);
   }
   static void k2(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
-    if constexpr (PT)
-      k_fused_pt<N, NH, DO, ACT, 1><<<grid, kPT, sm, s>>>(a);
-    else
-      k_fused<N, NH, DO, ACT, 1, T><<<grid, T, sm, s>>>(a);
+    k_fused<N, NH, DO, ACT, 1, T><<<grid, T, sm, s>>>(a);
   }
   static void kf(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
-    if constexpr (!PT) k_fused<N, NH, DO, ACT, 2, T><<<grid, T, sm, s>>>(a);
+    k_fused<N, NH, DO, ACT, 2, T><<<grid, T, sm, s>>>(a);
   }
-  static void pred(const float* params, int pstride, float sn, const float* pts, const int32_t* own, int64_t n,
+  static void pred(const float* params, int pstride, float sn, const float* pts, const Geo& geo, int64_t n,
                    float* out, const int32_t* sub_act, cudaStream_t s) {
     const int bs = 128;
     const int64_t g = (n + bs - 1) / bs;
-    if (g > 0)
-      k_predict<N, NH, DO, ACT><<<unsigned(g), bs, 0, s>>>(params, pstride, sn, pts, own, n, out, sub_act);
+    if (g > 0) k_predict<N, NH, DO, ACT><<<unsigned(g), bs, 0, s>>>(params, pstride, sn, pts, geo, n, out, sub_act);
   }
   // packed index -> internal offset (layer-major W, b, a)
   static void packmap(std::vector<int32_t>& m) {
@@ -104,44 +148,32 @@ struct Inst {
   }
   static cudaError_t setattr(size_t sm) {
     const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    cudaError_t e;
-    if constexpr (PT) {
-      e = cudaFuncSetAttribute(k_fused_pt<N, NH, DO, ACT, 0>, attr, int(sm));
-      if (e != cudaSuccess) return e;
-      return cudaFuncSetAttribute(k_fused_pt<N, NH, DO, ACT, 1>, attr, int(sm));
-    } else {
-      const auto carve = cudaFuncAttributePreferredSharedMemoryCarveout;
-      e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, attr, int(sm));
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, carve, 100);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, carve, 100);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 2, T>, carve, 100);
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 2, T>, attr, int(sm));
-      if (e != cudaSuccess) return e;
-      return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, attr, int(sm));
-    }
+    const auto carve = cudaFuncAttributePreferredSharedMemoryCarveout;
+    cudaError_t e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, attr, int(sm));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 0, T>, carve, 100);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, carve, 100);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 2, T>, carve, 100);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 2, T>, attr, int(sm));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_fused<N, NH, DO, ACT, 1, T>, attr, int(sm));
   }
   static Ops ops() {
     static_assert(NH <= kMaxHidden, "too many hidden layers");
-    if constexpr (PT) static_assert(PtCfg<N, NH, DO>::P == C::P, "both kernels tile by the same point count");
-    return Ops{N, NH, DO, ACT, PT ? 1 : 0, LY::total(), C::P, PT ? kPT : T, PT ? 1 : C::CPS, smem(), &k1, &k2,
-               PT ? nullptr : &kf, &pred, &packmap, &slopetab, &setattr};
+    return Ops{N, NH, DO, ACT, LY::total(), C::P, T, C::CPS, smem(), &k1, &k2, &kf, &pred, &packmap, &slopetab,
+               &setattr};
   }
 };
 
 // The shapes of BASELINE.json configs C1-C4 (tanh): 3x20, 5x20, 6x40, 5x80 (D_o = 3);
 // C5 (inverse heat, outputs (T, K)): 3x80 with tanh / sin / cos per region (Table 3).
-// Width-20 nets also have the point-per-thread kernel (pt = 1), selected with
-// PINN_DD_FLAG_POINT_PER_THREAD; the neuron-block kernel is the default (faster
-// on the B200).
-const Ops* find_ops(int N, int NH, int DO, int ACT, int pt = -1) {
+const Ops* find_ops(int N, int NH, int DO, int ACT) {
   static const Ops table[] = {
-      Inst<20, 3, 1, 0, true>::ops(),        Inst<20, 5, 1, 0, true>::ops(),
       // width 20: two 128-thread CTAs per SM (C3 K1 0.369 -> 0.285 ms)
-      Inst<20, 3, 1, 0, false, 128>::ops(),  Inst<20, 5, 1, 0, false, 128>::ops(),
-      Inst<20, 3, 1, 0>::ops(),              Inst<20, 5, 1, 0>::ops(),
+      Inst<20, 3, 1, 0, 128>::ops(),  Inst<20, 5, 1, 0, 128>::ops(),
+      Inst<20, 3, 1, 0>::ops(),       Inst<20, 5, 1, 0>::ops(),
       // width 40: two 128-thread CTAs per SM as well (C2 K1 1.443 -> 1.423 ms since the
       // coalesced chunk-partial read-modify-write; it was 1.65 vs 1.55 ms before)
-      Inst<40, 6, 1, 0, false, 128>::ops(),  Inst<40, 6, 1, 0>::ops(),
+      Inst<40, 6, 1, 0, 128>::ops(),  Inst<40, 6, 1, 0>::ops(),
       // width 80: one 256-thread CTA per SM (the weights alone are 104 KB of shared memory)
       Inst<80, 5, 3, 0>::ops(),              Inst<80, 3, 2, kActMixed>::ops(),
   };
@@ -150,9 +182,9 @@ const Ops* find_ops(int N, int NH, int DO, int ACT, int pt = -1) {
   const int thr = ev ? std::atoi(ev) : 0;
   const Ops* first = nullptr;
   for (const Ops& o : table)
-    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT && (pt < 0 || o.pt == pt)) {
+    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT) {
       if (!first) first = &o;
-      if (thr == 0 || o.pt || o.threads == thr) return &o;
+      if (thr == 0 || o.threads == thr) return &o;
     }
   return first;
 }
@@ -166,6 +198,22 @@ struct pinn_dd {
   std::vector<int64_t> seg_twin;
   std::vector<float> seg_normal;
   std::vector<pinn_dd_hparams> hp;
+  // exchange plan (Algorithm 1 green stage): per peer rank, the local rows sent
+  // and the received row range
+  std::vector<int32_t> peer_rank;
+  std::vector<int64_t> peer_send_off, send_rows, peer_recv_row, peer_recv_n;
+  ncclComm_t comm = nullptr;
+  cudaStream_t cstream = nullptr;       // exchange stream (forked from / joined to the step's stream)
+  cudaEvent_t xfork = nullptr, xjoin = nullptr;
+  float* sendbuf = nullptr;
+  int32_t* psend = nullptr;
+  // Eq. (4) geometry
+  std::vector<float> geo;               // boxes [n_geo][4] or seeds [n_geo][2]
+  std::vector<float> poly;              // [n_poly][2]
+  std::vector<int32_t> geo_local;       // [n_geo] local subdomain of each geometry entry, -1 = remote
+  float* dgeo = nullptr;
+  float* dpoly = nullptr;
+  int32_t* dgeo_local = nullptr;
   const Ops* ops = nullptr;
   int nf = 0, neq = 0, n_packed = 0, pstride = 0;
   int nsm = 148;
@@ -177,7 +225,7 @@ struct pinn_dd {
   float *pinv = nullptr, *gstash = nullptr, *scratch = nullptr;
   int32_t *pinfo = nullptr, *ptwin = nullptr, *sub_chunk = nullptr, *tstep = nullptr, *done = nullptr;
   double* slope_part = nullptr;
-  int32_t *flag = nullptr, *packmap = nullptr, *sub_act = nullptr, *order1 = nullptr, *sched = nullptr;
+  int32_t *sflag = nullptr, *packmap = nullptr, *sub_act = nullptr, *order1 = nullptr, *sched = nullptr;
   float2* segn = nullptr;
   float4 *sub_w = nullptr, *sub_adam = nullptr;
   Chunk *chunks1 = nullptr, *chunks2 = nullptr;
@@ -186,9 +234,10 @@ struct pinn_dd {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t gstream = nullptr;
   cudaEvent_t gjoin[2] = {};
-  // timing
-  cudaEvent_t ev[6] = {};
-  double ms[3] = {0, 0, 0};
+  // timing: ev[0..6] step events (see one_iteration), ev[7], ev[8] phased calls;
+  // ms = {K2, K1, K5, -, exchange, K1 interior, K1 interface, exposed exchange wait}
+  cudaEvent_t ev[9] = {};
+  double ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long launches = 0;
   std::string err;
 };
@@ -278,7 +327,7 @@ struct Carve {
 struct Layout {
   size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ord1,
       sched, ch2, subch,
-      tstep, done, flag, loss, packmap, slopep, gstash, total;
+      tstep, done, sflag, loss, packmap, slopep, sendbuf, psend, dgeo, dpoly, dgeoloc, gstash, total;
 };
 
 // validation + planning shared by workspace_size and create
@@ -301,12 +350,8 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   }
   const int act0 = d->sub_activation ? d->sub_activation[0] : d->activation;
   // one compiled activation if uniform, else the per-subdomain (kActMixed) instance
-  const int want_pt = (d->flags & PINN_DD_FLAG_POINT_PER_THREAD) ? 1 : 0;
-  const Ops* ops = nullptr;
-  for (int pt = want_pt; pt >= 0 && !ops; --pt) {   // no point-per-thread instance: neuron blocks
-    ops = mixed ? nullptr : find_ops(d->width, d->n_hidden, d->d_out, act0, pt);
-    if (!ops) ops = find_ops(d->width, d->n_hidden, d->d_out, kActMixed, pt);
-  }
+  const Ops* ops = mixed ? nullptr : find_ops(d->width, d->n_hidden, d->d_out, act0);
+  if (!ops) ops = find_ops(d->width, d->n_hidden, d->d_out, kActMixed);
   if (!ops)
     return fail(h, PINN_DD_EUNSUPPORTED, "network [2, %dx%d, %d] activation %d%s not compiled in", d->width,
                 d->n_hidden, d->d_out, act0, mixed ? " (mixed per subdomain)" : "");
@@ -361,6 +406,47 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
       return fail(h, PINN_DD_EPROTOCOL, "segment %d: twin rows [%lld, +%d) out of range", s, (long long)tw,
                   d->seg_n[s]);
   }
+  // exchange plan: peers' received ranges tile [n_points, n_points + n_recv)
+  // in peer order; sent rows are local interface points (checked in create)
+  if (d->n_peers < 0 || (d->n_peers > 0 && (!d->peer_rank || !d->peer_send_off || !d->peer_recv_row ||
+                                            !d->peer_recv_n || (!d->send_rows && d->peer_send_off[d->n_peers] > 0))))
+    return fail(h, PINN_DD_EPROTOCOL, "exchange plan arrays must not be NULL (n_peers = %d)", d->n_peers);
+  int64_t n_send = 0;
+  {
+    int64_t row = d->n_points;
+    if (d->n_peers > 0 && d->peer_send_off[0] != 0) return fail(h, PINN_DD_EPROTOCOL, "peer_send_off[0] != 0");
+    for (int i = 0; i < d->n_peers; ++i) {
+      if (i > 0 && d->peer_rank[i] <= d->peer_rank[i - 1])
+        return fail(h, PINN_DD_EPROTOCOL, "peer ranks must be distinct and ascending");
+      if (d->nccl_id && (d->peer_rank[i] < 0 || d->peer_rank[i] >= d->world))
+        return fail(h, PINN_DD_EPROTOCOL, "peer rank %d outside the communicator of %d", d->peer_rank[i], d->world);
+      if (d->peer_send_off[i + 1] < d->peer_send_off[i])
+        return fail(h, PINN_DD_EPROTOCOL, "peer_send_off not monotone");
+      if (d->peer_recv_row[i] != row || d->peer_recv_n[i] < 0)
+        return fail(h, PINN_DD_EPROTOCOL, "peer %d: received rows must start at %lld", i, (long long)row);
+      row += d->peer_recv_n[i];
+    }
+    if (row != d->n_points + d->n_recv)
+      return fail(h, PINN_DD_EPROTOCOL, "received rows cover %lld of n_recv = %lld", (long long)(row - d->n_points),
+                  (long long)d->n_recv);
+    if (d->n_peers > 0) n_send = d->peer_send_off[d->n_peers];
+    for (int64_t j = 0; j < n_send; ++j)
+      if (d->send_rows[j] < 0 || d->send_rows[j] >= d->n_points)
+        return fail(h, PINN_DD_EPROTOCOL, "send row %lld out of range", (long long)d->send_rows[j]);
+  }
+  if (d->nccl_id && (d->world < 1 || d->rank < 0 || d->rank >= d->world))
+    return fail(h, PINN_DD_EINVAL, "rank %d / world %d", d->rank, d->world);
+  // Eq. (4) geometry
+  if (d->geometry < 0 || d->geometry > 2) return fail(h, PINN_DD_EINVAL, "bad geometry %d", d->geometry);
+  if (d->geometry != PINN_DD_GEOM_NONE) {
+    if (d->n_geo < 1 || !d->geo || !d->geo_local) return fail(h, PINN_DD_EINVAL, "geometry arrays must not be NULL");
+    if (d->geometry == PINN_DD_GEOM_VORONOI && (d->n_poly < 3 || !d->poly))
+      return fail(h, PINN_DD_EINVAL, "Voronoi geometry needs a polygon of >= 3 vertices");
+    if (!(d->geo_tol >= 0.0f)) return fail(h, PINN_DD_EINVAL, "geo_tol must be >= 0");
+    for (int g = 0; g < d->n_geo; ++g)
+      if (d->geo_local[g] < -1 || d->geo_local[g] >= d->n_sub)
+        return fail(h, PINN_DD_EINVAL, "geo_local[%d] = %d out of range", g, d->geo_local[g]);
+  }
   // tiles and chunks.  The chunking of a subdomain depends only on its own
   // point count (never on which other subdomains share the GPU), so the
   // fixed-order reduction is bitwise placement-invariant.
@@ -402,10 +488,16 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->subch = c.take<int32_t>(ns + 1);
   L->tstep = c.take<int32_t>(ns);
   L->done = c.take<int32_t>(ns);
-  L->flag = c.take<int32_t>(1);
+  L->sflag = c.take<int32_t>(ns);
   L->loss = c.take<float>(ns * 8);
   L->packmap = c.take<int32_t>(size_t(pstride));
   L->slopep = c.take<double>(ns * size_t((pstride + kRB - 1) / kRB) * kMaxHidden);
+  L->sendbuf = c.take<float>(size_t(n_send + 1) * nf);
+  L->psend = c.take<int32_t>(npt + 1);
+  const int ngeo = d->geometry ? d->n_geo : 0;
+  L->dgeo = c.take<float>(size_t(ngeo) * 4 + 4);
+  L->dpoly = c.take<float>(size_t(d->geometry == PINN_DD_GEOM_VORONOI ? d->n_poly : 0) * 2 + 2);
+  L->dgeoloc = c.take<int32_t>(size_t(ngeo) + 1);
   L->gstash = (d->flags & PINN_DD_FLAG_GLOBAL_STASH)
                   ? c.take<float>(size_t(grid1) * d->n_hidden * kA * ops->threads)
                   : c.off;
@@ -454,6 +546,8 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.partial = h->partial;
   a.partial_loss = h->partial_loss;
   a.payload = h->payload;
+  a.psend = h->send_rows.empty() ? nullptr : h->psend;
+  a.sendbuf = h->sendbuf;
   a.gstash = (d.flags & PINN_DD_FLAG_GLOBAL_STASH) ? h->gstash : nullptr;
   a.pc.pde = d.pde;
   a.pc.nu = d.nu;
@@ -481,7 +575,7 @@ RArgs make_rargs(pinn_dd* h, int mode) {
   r.sub_w = h->sub_w;
   r.sub_adam = h->sub_adam;
   r.loss = h->loss;
-  r.flag = h->flag;
+  r.sflag = h->sflag;
   r.slope_part = h->slope_part;
   r.mode = mode;
   h->ops->slopetab(r);
@@ -517,12 +611,13 @@ pinn_dd_status launch_k1(pinn_dd* h, int part = 0) {
 pinn_dd_status launch_k5(pinn_dd* h, int mode) {
   dim3 g((h->pstride + kRB - 1) / kRB, h->d.n_sub);
   if (mode != 2) {
+    // status bits of this evaluation start at 0 (loss column 5)
+    CK(h, cudaMemsetAsync(h->sflag, 0, size_t(h->d.n_sub) * 4, h->stream));
     k_reduce<<<g, kRB, 0, h->stream>>>(make_rargs(h, 0));
     ++h->launches;
     CK(h, cudaGetLastError());
   }
-  RArgs r = make_rargs(h, mode == 0 ? 0 : 1);
-  if (mode == 2) r.n_hidden = 0;   // slopes were filled by pinn_dd_loss_grad
+  RArgs r = make_rargs(h, mode);   // 2: Adam on the stored gradient (slopes were filled by loss_grad)
   k_slope_adam<<<g, kRB, 0, h->stream>>>(r);
   ++h->launches;
   CK(h, cudaGetLastError());
@@ -531,23 +626,38 @@ pinn_dd_status launch_k5(pinn_dd* h, int mode) {
 
 // record = event timestamps around K2 / K1 / K5 (as external event-record
 // nodes when captured into the step graph)
-pinn_dd_status record(pinn_dd* h, int i, bool capturing) {
+pinn_dd_status record(pinn_dd* h, int i, bool capturing, cudaStream_t st = nullptr) {
+  if (!st) st = h->stream;
   if (capturing)
-    CK(h, cudaEventRecordWithFlags(h->ev[i], h->stream, cudaEventRecordExternal));
+    CK(h, cudaEventRecordWithFlags(h->ev[i], st, cudaEventRecordExternal));
   else
-    CK(h, cudaEventRecord(h->ev[i], h->stream));
+    CK(h, cudaEventRecord(h->ev[i], st));
   return PINN_DD_OK;
 }
 
-pinn_dd_status accumulate_times(pinn_dd* h, bool fused = false) {
+float elapsed(pinn_dd* h, int a, int b) {
+  float ms = 0.0f;
+  return cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]) == cudaSuccess ? ms : 0.0f;
+}
+
+// kind 0: K2 -> K1 -> K5 (events 0..3); 1: fused K2+K1 -> K5 (1..3);
+// 2: distributed (0..6, see one_iteration)
+pinn_dd_status accumulate_times(pinn_dd* h, int kind) {
   CK(h, cudaEventSynchronize(h->ev[3]));
-  float a = 0, b = 0, c = 0;
-  if (!fused) CK(h, cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
-  CK(h, cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
-  CK(h, cudaEventElapsedTime(&c, h->ev[2], h->ev[3]));
-  h->ms[0] += a;
-  h->ms[1] += b;
-  h->ms[2] += c;
+  if (kind == 2) {
+    h->ms[0] += elapsed(h, 0, 1);
+    const double in = elapsed(h, 1, 2), ifc = elapsed(h, 6, 5);
+    h->ms[1] += in + ifc;
+    h->ms[2] += elapsed(h, 5, 3);
+    h->ms[4] += elapsed(h, 1, 4);
+    h->ms[5] += in;
+    h->ms[6] += ifc;
+    h->ms[7] += elapsed(h, 2, 6);
+    return PINN_DD_OK;
+  }
+  if (kind == 0) h->ms[0] += elapsed(h, 0, 1);
+  h->ms[1] += elapsed(h, 1, 2);
+  h->ms[2] += elapsed(h, 2, 3);
   return PINN_DD_OK;
 }
 
@@ -563,13 +673,63 @@ pinn_dd_status launch_fused(pinn_dd* h) {
   return PINN_DD_OK;
 }
 
+bool remote(const pinn_dd* h) { return !h->peer_rank.empty(); }
+
 bool use_fused(const pinn_dd* h) {
   static const bool off = std::getenv("PINN_DD_NO_FUSED_STEP") != nullptr;   // development A/B knob
-  return h->ops->kf && h->n_chunks2 > 0 && h->d.n_recv == 0 && !off;
+  return h->ops->kf && h->n_chunks2 > 0 && h->d.n_recv == 0 && !remote(h) && !off;
+}
+
+#define CKN(h, call)                                                                                         \
+  do {                                                                                                       \
+    const ncclResult_t r_ = (call);                                                                          \
+    if (r_ != 0) return fail(h, PINN_DD_ENCCL, "%s: %s", #call, nccl().GetErrorString(r_));                 \
+  } while (0)
+
+// the green stage on stream `st`: one NCCL group of every peer's send (the
+// rows K2 wrote to the send buffer) and receive (straight into the payload
+// buffer's received rows)
+pinn_dd_status nccl_group(pinn_dd* h, cudaStream_t st) {
+  const Nccl& N = nccl();
+  const size_t nf = size_t(h->nf);
+  CKN(h, N.GroupStart());
+  for (size_t i = 0; i < h->peer_rank.size(); ++i) {
+    const int64_t s0 = h->peer_send_off[i], sn = h->peer_send_off[i + 1] - s0;
+    if (sn > 0) CKN(h, N.Send(h->sendbuf + size_t(s0) * nf, size_t(sn) * nf, kNcclFloat32, h->peer_rank[i], h->comm, st));
+    if (h->peer_recv_n[i] > 0)
+      CKN(h, N.Recv(h->payload + size_t(h->peer_recv_row[i]) * nf, size_t(h->peer_recv_n[i]) * nf, kNcclFloat32,
+                    h->peer_rank[i], h->comm, st));
+  }
+  CKN(h, N.GroupEnd());
+  return PINN_DD_OK;
 }
 
 pinn_dd_status one_iteration(pinn_dd* h, bool timed, bool capturing) {
   pinn_dd_status s;
+  if (remote(h)) {
+    // Algorithm 1 with remote neighbours: K2 -> [exchange stream: NCCL group]
+    // || K1 over residual + training points -> wait -> K1 over interface
+    // points -> K5.  Events: 0 before K2, 1 after K2, 4 exchange done (exchange
+    // stream), 2 after K1 interior, 6 after the wait, 5 after K1 interface, 3 after K5.
+    if (timed && (s = record(h, 0, capturing)) != PINN_DD_OK) return s;
+    if ((s = launch_k2(h)) != PINN_DD_OK) return s;
+    if (timed && (s = record(h, 1, capturing)) != PINN_DD_OK) return s;
+    CK(h, cudaEventRecord(h->xfork, h->stream));
+    CK(h, cudaStreamWaitEvent(h->cstream, h->xfork, 0));
+    if ((s = nccl_group(h, h->cstream)) != PINN_DD_OK) return s;
+    if (timed && (s = record(h, 4, capturing, h->cstream)) != PINN_DD_OK) return s;
+    CK(h, cudaEventRecord(h->xjoin, h->cstream));
+    if ((s = launch_k1(h, 1)) != PINN_DD_OK) return s;
+    if (timed && (s = record(h, 2, capturing)) != PINN_DD_OK) return s;
+    CK(h, cudaStreamWaitEvent(h->stream, h->xjoin, 0));
+    if (timed && (s = record(h, 6, capturing)) != PINN_DD_OK) return s;
+    if ((s = launch_k1(h, 2)) != PINN_DD_OK) return s;
+    if (timed && (s = record(h, 5, capturing)) != PINN_DD_OK) return s;
+    if ((s = launch_k5(h, 1)) != PINN_DD_OK) return s;
+    if (timed && (s = record(h, 3, capturing)) != PINN_DD_OK) return s;
+    if (timed && !capturing) return accumulate_times(h, 2);
+    return PINN_DD_OK;
+  }
   if (timed && !use_fused(h) && (s = record(h, 0, capturing)) != PINN_DD_OK) return s;
   if (use_fused(h)) {
     // K2 folded into K1 (reported as 0 ms); three event nodes, not four: each
@@ -579,7 +739,7 @@ pinn_dd_status one_iteration(pinn_dd* h, bool timed, bool capturing) {
     if (timed && (s = record(h, 2, capturing)) != PINN_DD_OK) return s;
     if ((s = launch_k5(h, 1)) != PINN_DD_OK) return s;
     if (timed && (s = record(h, 3, capturing)) != PINN_DD_OK) return s;
-    if (timed && !capturing) return accumulate_times(h, true);
+    if (timed && !capturing) return accumulate_times(h, 1);
     return PINN_DD_OK;
   }
   if ((s = launch_k2(h)) != PINN_DD_OK) return s;
@@ -588,7 +748,28 @@ pinn_dd_status one_iteration(pinn_dd* h, bool timed, bool capturing) {
   if (timed && (s = record(h, 2, capturing)) != PINN_DD_OK) return s;
   if ((s = launch_k5(h, 1)) != PINN_DD_OK) return s;
   if (timed && (s = record(h, 3, capturing)) != PINN_DD_OK) return s;
-  if (timed && !capturing) return accumulate_times(h);
+  if (timed && !capturing) return accumulate_times(h, 0);
+  return PINN_DD_OK;
+}
+
+int timing_kind(const pinn_dd* h) { return remote(h) ? 2 : (use_fused(h) ? 1 : 0); }
+
+// launches per iteration (as counted by the graph replay)
+int iteration_launches(const pinn_dd* h) {
+  if (remote(h)) return (h->n_chunks2 > 0) + (h->n_int > 0) + (h->n_chunks1 - h->n_int > 0) + 2;
+  return use_fused(h) ? 3 : (h->n_chunks2 > 0 ? 4 : 3);
+}
+
+// loss column 5 holds the status bits of the last evaluation (kFlag*)
+pinn_dd_status check_status(pinn_dd* h, const float* loss_host) {
+  for (int q = 0; q < h->d.n_sub; ++q) {
+    const int f = int(loss_host[q * 8 + 5]);
+    if (f & kFlagJ) return fail(h, PINN_DD_ENONFINITE, "non-finite J in subdomain %d", q);
+    if (f & kFlagGrad) return fail(h, PINN_DD_ENONFINITE, "non-finite W/b gradient in subdomain %d", q);
+    if (f & kFlagSlopeZero)
+      return fail(h, PINN_DD_ENONFINITE, "slope a^k = 0 in subdomain %d: its gradient is undefined (NaN)", q);
+    if (f & kFlagSlopeGrad) return fail(h, PINN_DD_ENONFINITE, "non-finite slope gradient in subdomain %d", q);
+  }
   return PINN_DD_OK;
 }
 
@@ -658,6 +839,27 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   else
     h->act.assign(ns, d->activation);
   h->d.sub_activation = h->act.data();
+  if (d->n_peers > 0) {
+    h->peer_rank.assign(d->peer_rank, d->peer_rank + d->n_peers);
+    h->peer_send_off.assign(d->peer_send_off, d->peer_send_off + d->n_peers + 1);
+    h->send_rows.assign(d->send_rows, d->send_rows + h->peer_send_off.back());
+    h->peer_recv_row.assign(d->peer_recv_row, d->peer_recv_row + d->n_peers);
+    h->peer_recv_n.assign(d->peer_recv_n, d->peer_recv_n + d->n_peers);
+  }
+  h->d.peer_rank = h->peer_rank.data();
+  h->d.peer_send_off = h->peer_send_off.data();
+  h->d.send_rows = h->send_rows.data();
+  h->d.peer_recv_row = h->peer_recv_row.data();
+  h->d.peer_recv_n = h->peer_recv_n.data();
+  h->d.nccl_id = nullptr;   // consumed below (the communicator is the handle's)
+  if (d->geometry != PINN_DD_GEOM_NONE) {
+    h->geo.assign(d->geo, d->geo + size_t(d->n_geo) * (d->geometry == PINN_DD_GEOM_BOXES ? 4 : 2));
+    h->geo_local.assign(d->geo_local, d->geo_local + d->n_geo);
+    if (d->geometry == PINN_DD_GEOM_VORONOI) h->poly.assign(d->poly, d->poly + 2 * size_t(d->n_poly));
+  }
+  h->d.geo = h->geo.data();
+  h->d.geo_local = h->geo_local.data();
+  h->d.poly = h->poly.data();
   h->stream = static_cast<cudaStream_t>(d->stream);
 
   char* base = static_cast<char*>(ws);
@@ -683,11 +885,16 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->sub_chunk = reinterpret_cast<int32_t*>(base + L.subch);
   h->tstep = reinterpret_cast<int32_t*>(base + L.tstep);
   h->done = reinterpret_cast<int32_t*>(base + L.done);
-  h->flag = reinterpret_cast<int32_t*>(base + L.flag);
+  h->sflag = reinterpret_cast<int32_t*>(base + L.sflag);
   h->slope_part = reinterpret_cast<double*>(base + L.slopep);
   h->loss = reinterpret_cast<float*>(base + L.loss);
   h->packmap = reinterpret_cast<int32_t*>(base + L.packmap);
   h->gstash = reinterpret_cast<float*>(base + L.gstash);
+  h->sendbuf = reinterpret_cast<float*>(base + L.sendbuf);
+  h->psend = reinterpret_cast<int32_t*>(base + L.psend);
+  h->dgeo = reinterpret_cast<float*>(base + L.dgeo);
+  h->dpoly = reinterpret_cast<float*>(base + L.dpoly);
+  h->dgeo_local = reinterpret_cast<int32_t*>(base + L.dgeoloc);
 
   // ---- per-point classification and 1/N (Eq. 3/5/6; per-edge mean, Z2)
   const int64_t np = d->n_points;
@@ -721,18 +928,46 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
       }
     }
   }
-  // a local twin must itself be an interface point
-  for (int sgi = 0; sgi < d->n_seg; ++sgi) {
-    const int64_t tw = h->seg_twin[sgi];
-    if (tw < np) {
-      for (int j = 0; j < h->seg_n[sgi]; ++j)
-        if ((pinfo[tw + j] & 3) != 2) {
-          s = fail(nullptr, PINN_DD_EPROTOCOL, "segment %d: twin row %lld is not an interface point", sgi,
-                   (long long)(tw + j));
-          delete h;
-          return s;
-        }
+  // a local twin must be the first point of another segment of the same
+  // edge: same N_I, same interface condition, same canonical normal (Z3)
+  {
+    std::vector<int64_t> seg_start(d->n_seg);
+    for (int q = 0; q < ns; ++q) {
+      int64_t p0 = h->sub_off[q] + h->n_res[q] + h->n_data[q];
+      for (int sgi = h->seg_off[q]; sgi < h->seg_off[q + 1]; ++sgi) {
+        seg_start[sgi] = p0;
+        p0 += h->seg_n[sgi];
+      }
     }
+    for (int sgi = 0; sgi < d->n_seg; ++sgi) {
+      const int64_t tw = h->seg_twin[sgi];
+      if (tw >= np) continue;   // received rows: validated by the sender's plan
+      const int32_t info = pinfo[tw];
+      const int ts = (info & 3) == 2 ? (info >> 3) : -1;
+      const char* why = nullptr;
+      if (ts < 0 || seg_start[ts] != tw) why = "is not the first point of an interface segment";
+      else if (ts == sgi) why = "is the segment itself";
+      else if (h->seg_n[ts] != h->seg_n[sgi]) why = "belongs to a segment with a different N_I";
+      else if ((pinfo[tw] & 4) != (pinfo[seg_start[sgi]] & 4)) why = "belongs to a segment with another condition";
+      else if (h->seg_normal[2 * ts] != h->seg_normal[2 * sgi] || h->seg_normal[2 * ts + 1] != h->seg_normal[2 * sgi + 1])
+        why = "belongs to a segment with another normal";
+      if (why) {
+        s = fail(nullptr, PINN_DD_EPROTOCOL, "segment %d: twin row %lld %s", sgi, (long long)tw, why);
+        delete h;
+        return s;
+      }
+    }
+  }
+  // send slot of every point of a cut edge (K2 writes its payload row there too)
+  std::vector<int32_t> psend(np + 1, -1);
+  for (size_t j = 0; j < h->send_rows.size(); ++j) {
+    const int64_t r = h->send_rows[j];
+    if ((pinfo[r] & 3) != 2 || psend[r] != -1) {
+      s = fail(nullptr, PINN_DD_EPROTOCOL, "send row %lld is not an interface point or is sent twice", (long long)r);
+      delete h;
+      return s;
+    }
+    psend[r] = int32_t(j);
   }
   std::vector<float4> subw(ns), suba(ns);
   for (int q = 0; q < ns; ++q) {
@@ -796,6 +1031,8 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   CKC(cudaMemsetAsync(h->v, 0, pbytes, st));
   CKC(cudaMemsetAsync(h->grad, 0, pbytes, st));
   CKC(cudaMemsetAsync(h->payload, 0, (size_t(np) + d->n_recv + 1) * h->nf * sizeof(float), st));
+  // K1 never writes a partial's padding slots; K5a sums every index, so they start (and stay) 0
+  CKC(cudaMemsetAsync(h->partial, 0, size_t(h->n_chunks1) * h->pstride * sizeof(float), st));
   CKC(cudaMemcpyAsync(h->pinfo, pinfo.data(), pinfo.size() * 4, cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->pinv, pinv.data(), pinv.size() * 4, cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->ptwin, ptwin.data(), ptwin.size() * 4, cudaMemcpyHostToDevice, st));
@@ -812,17 +1049,73 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   CKC(cudaMemcpyAsync(h->sub_chunk, subch.data(), subch.size() * 4, cudaMemcpyHostToDevice, st));
   CKC(cudaMemsetAsync(h->tstep, 0, ns * 4, st));
   CKC(cudaMemsetAsync(h->done, 0, ns * 4, st));
-  CKC(cudaMemsetAsync(h->flag, 0, 4, st));
+  CKC(cudaMemsetAsync(h->sflag, 0, ns * 4, st));
   CKC(cudaMemsetAsync(h->loss, 0, ns * 8 * 4, st));
   CKC(cudaMemcpyAsync(h->packmap, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice, st));
-  if (d->init_params) {
+  CKC(cudaMemcpyAsync(h->psend, psend.data(), psend.size() * 4, cudaMemcpyHostToDevice, st));
+  if (!h->geo.empty()) {
+    CKC(cudaMemcpyAsync(h->dgeo, h->geo.data(), h->geo.size() * 4, cudaMemcpyHostToDevice, st));
+    CKC(cudaMemcpyAsync(h->dgeo_local, h->geo_local.data(), h->geo_local.size() * 4, cudaMemcpyHostToDevice, st));
+  }
+  if (!h->poly.empty()) CKC(cudaMemcpyAsync(h->dpoly, h->poly.data(), h->poly.size() * 4, cudaMemcpyHostToDevice, st));
+  {
+    // initial parameters: the caller's, or W = b = 0 with a^k = 1/n (Z6).  The
+    // slope gradient comes from a^k dJ/da^k = <W, dJ/dW> + <b, dJ/db> (DESIGN.md
+    // 5.3), which needs a^k != 0: a zero slope is rejected here.
+    std::vector<float> init(size_t(ns) * h->n_packed, 0.0f);
+    std::vector<int> slot_a;
+    for (int k = 0, o = 0; k < d->n_hidden; ++k) {
+      o += (k == 0 ? 2 : d->width) * d->width + d->width;
+      slot_a.push_back(o);
+      o += 1;
+    }
+    if (d->init_params) {
+      CKC(cudaMemcpyAsync(init.data(), d->init_params, init.size() * 4, cudaMemcpyDeviceToHost, st));
+      CKC(cudaStreamSynchronize(st));
+      for (int q = 0; q < ns; ++q)
+        for (int k = 0; k < d->n_hidden; ++k)
+          if (!(std::isfinite(init[size_t(q) * h->n_packed + slot_a[k]]) &&
+                init[size_t(q) * h->n_packed + slot_a[k]] != 0.0f)) {
+            fail(nullptr, PINN_DD_EINVAL, "subdomain %d: slope a^%d = %g must be finite and non-zero", q, k + 1,
+                 double(init[size_t(q) * h->n_packed + slot_a[k]]));
+            delete h;
+            return PINN_DD_EINVAL;
+          }
+    } else {
+      for (int q = 0; q < ns; ++q)
+        for (int k = 0; k < d->n_hidden; ++k) init[size_t(q) * h->n_packed + slot_a[k]] = 1.0f / d->slope_n;
+    }
+    CKC(cudaMemcpyAsync(h->scratch, init.data(), init.size() * 4, cudaMemcpyHostToDevice, st));
     dim3 g((h->n_packed + 255) / 256, ns);
-    k_scatter<<<g, 256, 0, st>>>(d->init_params, h->packmap, h->n_packed, h->pstride, h->n_packed, h->params, ns);
+    k_scatter<<<g, 256, 0, st>>>(h->scratch, h->packmap, h->n_packed, h->pstride, h->n_packed, h->params, ns);
     CKC(cudaGetLastError());
+    CKC(cudaStreamSynchronize(st));   // `init` goes out of scope
   }
   for (auto& e : h->ev) CKC(cudaEventCreate(&e));
   for (auto& e : h->gjoin) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CKC(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&h->xfork, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&h->xjoin, cudaEventDisableTiming));
+  if (d->nccl_id) {
+    // join the exchange communicator (collective over the `world` ranks)
+    const Nccl& N = nccl();
+    if (!N.ok) {
+      fail(nullptr, PINN_DD_ENCCL, "NCCL transport requested but unavailable: %s", N.why.c_str());
+      pinn_dd_destroy(h);
+      return PINN_DD_ENCCL;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, d->nccl_id, sizeof id);
+    const ncclResult_t r = N.CommInitRank(&h->comm, d->world, id, d->rank);
+    if (r != 0) {
+      h->comm = nullptr;
+      fail(nullptr, PINN_DD_ENCCL, "ncclCommInitRank(world %d, rank %d): %s", d->world, d->rank,
+           N.GetErrorString(r));
+      pinn_dd_destroy(h);
+      return PINN_DD_ENCCL;
+    }
+  }
   CKC(cudaStreamSynchronize(st));   // host vectors above go out of scope
   *out = h;
   return PINN_DD_OK;
@@ -830,16 +1123,17 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
 
 // per-call timing of the phased entry points (PINN_DD_FLAG_TIMING): events 4/5
 static pinn_dd_status phase_begin(pinn_dd* h) {
-  if (h->d.flags & PINN_DD_FLAG_TIMING) CK(h, cudaEventRecord(h->ev[4], h->stream));
+  if (h->d.flags & PINN_DD_FLAG_TIMING) CK(h, cudaEventRecord(h->ev[7], h->stream));
   return PINN_DD_OK;
 }
-static pinn_dd_status phase_end(pinn_dd* h, int slot) {
+static pinn_dd_status phase_end(pinn_dd* h, int slot, int slot2 = -1) {
   if (h->d.flags & PINN_DD_FLAG_TIMING) {
-    CK(h, cudaEventRecord(h->ev[5], h->stream));
-    CK(h, cudaEventSynchronize(h->ev[5]));
+    CK(h, cudaEventRecord(h->ev[8], h->stream));
+    CK(h, cudaEventSynchronize(h->ev[8]));
     float ms = 0;
-    CK(h, cudaEventElapsedTime(&ms, h->ev[4], h->ev[5]));
+    CK(h, cudaEventElapsedTime(&ms, h->ev[7], h->ev[8]));
     h->ms[slot] += ms;
+    if (slot2 >= 0) h->ms[slot2] += ms;
   }
   return PINN_DD_OK;
 }
@@ -887,13 +1181,13 @@ pinn_dd_status pinn_dd_loss_grad_interior(pinn_dd* h) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
   pinn_dd_status s;
   if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h, 1)) != PINN_DD_OK) return s;
-  return phase_end(h, 1);
+  return phase_end(h, 1, 5);
 }
 
 pinn_dd_status pinn_dd_loss_grad_interface(pinn_dd* h, float* loss_dev, float* grad_dev) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
   pinn_dd_status s;
-  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h, 2)) != PINN_DD_OK || (s = phase_end(h, 1)) != PINN_DD_OK)
+  if ((s = phase_begin(h)) != PINN_DD_OK || (s = launch_k1(h, 2)) != PINN_DD_OK || (s = phase_end(h, 1, 6)) != PINN_DD_OK)
     return s;
   return finish_loss_grad(h, loss_dev, grad_dev);
 }
@@ -907,8 +1201,10 @@ pinn_dd_status pinn_dd_adam(pinn_dd* h) {
 
 pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
-  if (h->d.n_recv > 0)
-    return fail(h, PINN_DD_EPROTOCOL, "pinn_dd_step needs all twins local (n_recv = %lld); use the phased calls",
+  if (remote(h) && !h->comm)
+    return fail(h, PINN_DD_EPROTOCOL,
+                "pinn_dd_step with remote twins (n_recv = %lld) needs the NCCL transport (desc nccl_id); "
+                "else use the phased calls",
                 (long long)h->d.n_recv);
   if (n_iters < 0) return fail(h, PINN_DD_EINVAL, "n_iters < 0");
   const bool timed = (h->d.flags & PINN_DD_FLAG_TIMING) != 0;
@@ -918,10 +1214,19 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
     if (graph) {
       if (!h->gexec) {
         cudaGraph_t g;
+        if (remote(h)) {
+          // NCCL connects peers lazily on the first send / receive (allocations,
+          // IPC mappings): one eager exchange before capture (every rank calls
+          // pinn_dd_step, so the peers take part; the rows it moves are
+          // rewritten by K2 before they are read)
+          if ((s = nccl_group(h, h->stream)) != PINN_DD_OK) return s;
+          CK(h, cudaStreamSynchronize(h->stream));
+        }
         const long long before = h->launches;
         cudaStream_t user = h->stream;
         h->stream = h->gstream;
-        cudaError_t e0 = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+        cudaError_t e0 = cudaStreamBeginCapture(
+            h->stream, remote(h) ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal);
         if (e0 != cudaSuccess) {
           h->stream = user;
           return fail(h, PINN_DD_ECUDA, "graph capture: %s", cudaGetErrorString(e0));
@@ -940,8 +1245,8 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
       CK(h, cudaGraphLaunch(h->gexec, h->gstream));
       CK(h, cudaEventRecord(h->gjoin[1], h->gstream));
       CK(h, cudaStreamWaitEvent(h->stream, h->gjoin[1], 0));
-      h->launches += use_fused(h) ? 3 : (h->n_chunks2 > 0 ? 4 : 3);
-      if (timed && (s = accumulate_times(h, use_fused(h))) != PINN_DD_OK) return s;
+      h->launches += iteration_launches(h);
+      if (timed && (s = accumulate_times(h, timing_kind(h))) != PINN_DD_OK) return s;
     } else if ((s = one_iteration(h, timed, false)) != PINN_DD_OK) {
       return s;
     }
@@ -949,23 +1254,31 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
   if (loss_host) {
     CK(h, cudaMemcpyAsync(loss_host, h->loss, size_t(h->d.n_sub) * 8 * 4, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
-    int flag = 0;
-    CK(h, cudaMemcpy(&flag, h->flag, 4, cudaMemcpyDeviceToHost));
-    if (flag) {
-      CK(h, cudaMemset(h->flag, 0, 4));
-      for (int q = 0; q < h->d.n_sub; ++q)
-        if (!(loss_host[q * 8 + 4] == loss_host[q * 8 + 4]) || loss_host[q * 8 + 5] != 0.0f)
-          return fail(h, PINN_DD_ENONFINITE, "non-finite J in subdomain %d", q);
-      return fail(h, PINN_DD_ENONFINITE, "non-finite gradient (flag %d)", flag);
-    }
+    return check_status(h, loss_host);
   }
   return PINN_DD_OK;
 }
 
-pinn_dd_status pinn_dd_predict(pinn_dd* h, const float* pts, const int32_t* owners, int64_t n, float* out) {
+pinn_dd_status pinn_dd_predict(pinn_dd* h, const float* pts, int64_t n, float* out, int32_t mode) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  if (n < 0 || (n > 0 && (!pts || !out))) return fail(h, PINN_DD_EINVAL, "bad predict arguments");
+  if (mode != PINN_DD_PREDICT_STITCHED && mode != PINN_DD_PREDICT_OWNER)
+    return fail(h, PINN_DD_EINVAL, "bad predict mode %d", mode);
+  if (h->d.geometry == PINN_DD_GEOM_NONE)
+    return fail(h, PINN_DD_EINVAL, "pinn_dd_predict needs desc geometry (or use pinn_dd_predict_owners)");
+  Geo g{h->d.geometry, mode, nullptr, h->d.n_geo, h->dgeo, h->dgeo_local, int(h->poly.size() / 2), h->dpoly,
+        h->d.geo_tol};
+  h->ops->pred(h->params, h->pstride, h->d.slope_n, pts, g, n, out, h->sub_act, h->stream);
+  ++h->launches;
+  CK(h, cudaGetLastError());
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_predict_owners(pinn_dd* h, const float* pts, const int32_t* owners, int64_t n, float* out) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
   if (n < 0 || (n > 0 && (!pts || !owners || !out))) return fail(h, PINN_DD_EINVAL, "bad predict arguments");
-  h->ops->pred(h->params, h->pstride, h->d.slope_n, pts, owners, n, out, h->sub_act, h->stream);
+  Geo g{0, 0, owners, 0, nullptr, nullptr, 0, nullptr, 0.0f};
+  h->ops->pred(h->params, h->pstride, h->d.slope_n, pts, g, n, out, h->sub_act, h->stream);
   ++h->launches;
   CK(h, cudaGetLastError());
   return PINN_DD_OK;
@@ -1010,15 +1323,31 @@ pinn_dd_status pinn_dd_get_step(pinn_dd* h, int32_t sub, int32_t* t) {
   return PINN_DD_OK;
 }
 
-pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms4) {
-  if (!h || !ms4) return fail(h, PINN_DD_EINVAL, "bad kernel_times arguments");
+pinn_dd_status pinn_dd_kernel_times(pinn_dd* h, double* ms8) {
+  if (!h || !ms8) return fail(h, PINN_DD_EINVAL, "bad kernel_times arguments");
   CK(h, cudaStreamSynchronize(h->stream));
-  ms4[0] = h->ms[0];
-  ms4[1] = h->ms[1];
-  ms4[2] = h->ms[2];
-  ms4[3] = double(h->launches);
-  h->ms[0] = h->ms[1] = h->ms[2] = 0.0;
+  for (int i = 0; i < 8; ++i) ms8[i] = h->ms[i];
+  ms8[3] = double(h->launches);
+  for (double& v : h->ms) v = 0.0;
   h->launches = 0;
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_exchange(pinn_dd* h) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  if (!remote(h)) return PINN_DD_OK;
+  if (!h->comm) return fail(h, PINN_DD_EPROTOCOL, "pinn_dd_exchange needs the NCCL transport (desc nccl_id)");
+  return nccl_group(h, h->stream);
+}
+
+pinn_dd_status pinn_dd_nccl_unique_id(void* id128) {
+  if (!id128) return fail(nullptr, PINN_DD_EINVAL, "id128 is NULL");
+  const Nccl& N = nccl();
+  if (!N.ok) return fail(nullptr, PINN_DD_ENCCL, "NCCL unavailable: %s", N.why.c_str());
+  ncclUniqueId id;
+  const ncclResult_t r = N.GetUniqueId(&id);
+  if (r != 0) return fail(nullptr, PINN_DD_ENCCL, "ncclGetUniqueId: %s", N.GetErrorString(r));
+  std::memcpy(id128, &id, sizeof id);
   return PINN_DD_OK;
 }
 
@@ -1063,6 +1392,10 @@ void pinn_dd_destroy(pinn_dd* h) {
   for (auto& e : h->gjoin)
     if (e) cudaEventDestroy(e);
   if (h->gstream) cudaStreamDestroy(h->gstream);
+  if (h->comm) nccl().CommDestroy(h->comm);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
+  if (h->xfork) cudaEventDestroy(h->xfork);
+  if (h->xjoin) cudaEventDestroy(h->xjoin);
   delete h;
 }
 

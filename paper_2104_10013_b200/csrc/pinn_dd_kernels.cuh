@@ -351,6 +351,15 @@ __device__ __forceinline__ void point_payload(const KArgs& a, int64_t gp, float 
 #pragma unroll
   for (int o = 0; o < DO; ++o) q[o] = U[o].x;
   for (int e = 0; e < ne; ++e) q[DO + e] = r[e];
+  // a point of a cut edge also goes to the send buffer of its neighbour's rank
+  // (the exchange reads it right after this kernel, Algorithm 1)
+  const int ss = a.psend ? a.psend[gp] : -1;
+  if (ss >= 0) {
+    float* w = a.sendbuf + size_t(ss) * NF;
+#pragma unroll
+    for (int o = 0; o < DO; ++o) w[o] = U[o].x;
+    for (int e = 0; e < ne; ++e) w[DO + e] = r[e];
+  }
 }
 
 // epilogue of one point (K1): its loss terms (Eq. 3/5/6; lsum = MSE_u, MSE_F,
@@ -842,6 +851,12 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
 constexpr int kMaxHidden = 8;
 constexpr int kRB = 256;
 
+// per-subdomain status bits (loss column 5)
+constexpr int kFlagJ = 1;          // J_q non-finite
+constexpr int kFlagGrad = 2;       // a W / b gradient entry non-finite
+constexpr int kFlagSlopeGrad = 4;  // a slope gradient non-finite
+constexpr int kFlagSlopeZero = 8;  // a^k == 0: the slope identity is undefined (gradient set to NaN)
+
 struct RArgs {
   const float* partial;
   const float* partial_loss;
@@ -856,13 +871,18 @@ struct RArgs {
   const float4* sub_w;        // loss weights
   const float4* sub_adam;     // lr, beta1, beta2, eps
   float* loss;                // [n_sub][8]
-  int32_t* flag;              // non-finite flag
+  int32_t* sflag;             // [n_sub] status bits of the current evaluation (zeroed before K5a)
   double* slope_part;         // [n_sub][gridDim.x][kMaxHidden] per-block slope partials (K5a -> K5b)
-  int mode;                   // k_slope_adam: 0 slopes only, 1 slopes + Adam
-  int n_hidden;               // 0: skip the slope pass
+  int mode;                   // k_slope_adam: 0 slopes only, 1 slopes + Adam, 2 Adam only
+  int n_hidden;               // 0: no slope parameters
   int offW[kMaxHidden], nW[kMaxHidden], offB[kMaxHidden], nB[kMaxHidden], offA[kMaxHidden];
 };
 
+// K5a: gradient of subdomain q (blockIdx.y) = sum of its chunk partials in
+// chunk order, accumulated in FP64 (the slope identity below is a cancelling
+// dot product of these sums, so their rounding matters).
+// Indices that are not parameters (16-B padding, slope slots) are never
+// written by K1; the partial region is zeroed once at create.
 __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
   __shared__ double red[kRB / 32];
   const int q = blockIdx.y;
@@ -871,7 +891,7 @@ __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
   const int i = i0 + tid;
   const int c0 = r.sub_chunk[q], c1 = r.sub_chunk[q + 1];
   const float* P = r.params + size_t(q) * r.pstride;
-  float g = 0.0f;
+  double g = 0.0;
   if (i < r.pstride) {
     // chunk order, 8 loads in flight per thread
     int c = c0;
@@ -880,15 +900,16 @@ __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = __ldcg(r.partial + size_t(c + u) * r.pstride + i);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) g += v[u];
+      for (int u = 0; u < 8; ++u) g += double(v[u]);
     }
-    for (; c < c1; ++c) g += __ldcg(r.partial + size_t(c) * r.pstride + i);
-    r.grad[size_t(q) * r.pstride + i] = g;
-    if (!isfinite(g)) atomicOr(r.flag, 2);
+    for (; c < c1; ++c) g += double(__ldcg(r.partial + size_t(c) * r.pstride + i));
+    const float gf = float(g);
+    r.grad[size_t(q) * r.pstride + i] = gf;
+    if (!isfinite(gf)) atomicOr(r.sflag + q, kFlagGrad);
   }
   // per-block partial sums of <W^k, dJ/dW^k> + <b^k, dJ/db^k> (fp64, fixed
-  // order) for the slope identity; K5b combines them (no cross-block reads of
-  // parameters that K5b's Adam updates)
+  // order, from the FP64 sums above) for the slope identity; K5b combines them
+  // (no cross-block reads of parameters that K5b's Adam updates)
   for (int k = 0; k < r.n_hidden; ++k) {
     const int w0 = r.offW[k], w1 = w0 + r.nW[k], b0 = r.offB[k], b1 = b0 + r.nB[k];
     double* slot = r.slope_part + (size_t(q) * gridDim.x + blockIdx.x) * kMaxHidden + k;
@@ -897,7 +918,7 @@ __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
       if (tid == 0) *slot = 0.0;
       continue;
     }
-    double acc = ((i >= w0 && i < w1) || (i >= b0 && i < b1)) ? double(P[i]) * double(g) : 0.0;
+    double acc = ((i >= w0 && i < w1) || (i >= b0 && i < b1)) ? double(P[i]) * g : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((tid & 31) == 0) red[tid >> 5] = acc;
@@ -911,30 +932,28 @@ __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
   }
   if (blockIdx.x == 0 && tid < 32) {
     // loss terms of subdomain q: lane l sums chunks c0 + l, c0 + l + 32, ...; fixed shuffle tree
-    float4 l4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    double l4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int c = c0 + tid; c < c1; c += 32) {
       const float4 v = __ldcg(reinterpret_cast<const float4*>(r.partial_loss) + c);
-      l4.x += v.x; l4.y += v.y; l4.z += v.z; l4.w += v.w;
+      l4[0] += v.x; l4[1] += v.y; l4[2] += v.z; l4[3] += v.w;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      l4.x += __shfl_xor_sync(0xffffffffu, l4.x, o);
-      l4.y += __shfl_xor_sync(0xffffffffu, l4.y, o);
-      l4.z += __shfl_xor_sync(0xffffffffu, l4.z, o);
-      l4.w += __shfl_xor_sync(0xffffffffu, l4.w, o);
-    }
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) l4[t] += __shfl_xor_sync(0xffffffffu, l4[t], o);
     if (tid == 0) {
       const float4 w = r.sub_w[q];
-      const float J = w.x * l4.x + w.y * l4.y + w.z * l4.z + w.w * l4.w;
+      const double J = double(w.x) * l4[0] + double(w.y) * l4[1] + double(w.z) * l4[2] + double(w.w) * l4[3];
       float* L = r.loss + size_t(q) * 8;
-      L[0] = l4.x; L[1] = l4.y; L[2] = l4.z; L[3] = l4.w; L[4] = J;
-      L[5] = isfinite(J) ? 0.0f : 1.0f;
+      L[0] = float(l4[0]); L[1] = float(l4[1]); L[2] = float(l4[2]); L[3] = float(l4[3]); L[4] = float(J);
       L[6] = 0.0f; L[7] = 0.0f;
-      if (!isfinite(J)) atomicOr(r.flag, 1);
+      if (!isfinite(L[4])) atomicOr(r.sflag + q, kFlagJ);
     }
   }
 }
 
+// K5b: slope gradients, then (mode 1, 2) the Adam step; the last block of a
+// subdomain publishes its status bits in loss column 5 (and advances t).
 __global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
   const int q = blockIdx.y;
   const int i0 = blockIdx.x * kRB;
@@ -942,40 +961,51 @@ __global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
   const float* P = r.params + size_t(q) * r.pstride;
   float* G = r.grad + size_t(q) * r.pstride;
   // slope gradients: the block owning a^k combines K5a's
-  // per-block partials in block order
-  if (tid < r.n_hidden) {
+  // per-block partials in block order.  a^k = 0 leaves the identity
+  // undefined: the gradient is set to NaN and flagged (never a silent 0).
+  if (r.mode != 2 && tid < r.n_hidden) {
     const int oa = r.offA[tid];
     if (oa >= i0 && oa < i0 + kRB) {
       double sum = 0.0;
       for (int b = 0; b < int(gridDim.x); ++b) sum += r.slope_part[(size_t(q) * gridDim.x + b) * kMaxHidden + tid];
-      const float ga = float(sum / double(P[oa]));
+      const double a = double(P[oa]);
+      float ga;
+      if (a == 0.0) {
+        ga = __int_as_float(0x7fc00000);
+        atomicOr(r.sflag + q, kFlagSlopeZero);
+      } else {
+        ga = float(sum / a);
+        if (!isfinite(ga)) atomicOr(r.sflag + q, kFlagSlopeGrad);
+      }
       G[oa] = ga;
-      if (!isfinite(ga)) atomicOr(r.flag, 4);
     }
   }
   __syncthreads();
-  if (r.mode == 0) return;
-  const int i = i0 + tid;
   const int t = r.tstep[q] + 1;
-  if (i < r.pstride) {
-    const float g = G[i];
-    const float4 ad = r.sub_adam[q];
-    const size_t k = size_t(q) * r.pstride + i;
-    const float mm = ad.y * r.m[k] + (1.0f - ad.y) * g;
-    const float vv = ad.z * r.v[k] + (1.0f - ad.z) * g * g;
-    r.m[k] = mm;
-    r.v[k] = vv;
-    const float mh = mm / (1.0f - powf(ad.y, float(t)));
-    const float vh = vv / (1.0f - powf(ad.z, float(t)));
-    r.params[k] -= ad.x * mh / (sqrtf(vh) + ad.w);
+  if (r.mode != 0) {
+    const int i = i0 + tid;
+    if (i < r.pstride) {
+      const float g = G[i];
+      const float4 ad = r.sub_adam[q];
+      const size_t k = size_t(q) * r.pstride + i;
+      const float mm = ad.y * r.m[k] + (1.0f - ad.y) * g;
+      const float vv = ad.z * r.v[k] + (1.0f - ad.z) * g * g;
+      r.m[k] = mm;
+      r.v[k] = vv;
+      const float mh = mm / (1.0f - powf(ad.y, float(t)));
+      const float vh = vv / (1.0f - powf(ad.z, float(t)));
+      r.params[k] -= ad.x * mh / (sqrtf(vh) + ad.w);
+    }
   }
-  // the last block of subdomain q advances its Adam step counter
+  // the last block of subdomain q publishes the status bits and (Adam) advances t
   __syncthreads();
   if (tid == 0) {
     __threadfence();
     const int prev = atomicAdd(&r.done[q], 1);
     if (prev == int(gridDim.x) - 1) {
-      r.tstep[q] = t;
+      __threadfence();
+      if (r.mode != 0) r.tstep[q] = t;
+      r.loss[size_t(q) * 8 + 5] = float(atomicOr(r.sflag + q, 0));
       r.done[q] = 0;
       __threadfence();
     }
@@ -996,10 +1026,85 @@ __global__ void k_scatter(const float* src, const int32_t* map, int n, int pstri
 }
 
 // ----------------------------------------------------------------------------
-// K6: value-only forward + Eq. (4) stitching
+// K6: value-only forward + Eq. (4) stitching.  The owners of a
+// point are the caller's list (kind 0) or classified here (kind 1 Cartesian
+// cells, kind 2 nearest-seed cells inside a polygon), in FP64.
 // ----------------------------------------------------------------------------
+struct Geo {
+  int kind;                 // 0 caller's owners, 1 boxes, 2 Voronoi
+  int owner_mode;           // 0 stitched (1/S), 1 lowest-id owner only
+  const int32_t* owners;    // kind 0: [n][4] local ids, -1 unused
+  int n_geo;
+  const float* geo;         // boxes [n_geo][4] / seeds [n_geo][2]
+  const int32_t* local;     // [n_geo] local subdomain, -1 = other rank
+  int n_poly;
+  const float* poly;        // [n_poly][2]
+  float tol;
+};
+
+// even-odd crossing test; points within 1e-9 of an edge count as inside
+__device__ __forceinline__ bool in_polygon(double x, double y, const float* P, int n) {
+  bool in = false;
+  for (int i = 0, j = n - 1; i < n; j = i++) {
+    const double xi = P[2 * i], yi = P[2 * i + 1], xj = P[2 * j], yj = P[2 * j + 1];
+    const double ex = xj - xi, ey = yj - yi;
+    const double l2 = ex * ex + ey * ey;
+    double t = l2 > 0.0 ? ((x - xi) * ex + (y - yi) * ey) / l2 : 0.0;
+    t = fmin(1.0, fmax(0.0, t));
+    const double dx = x - (xi + t * ex), dy = y - (yi + t * ey);
+    if (dx * dx + dy * dy <= 1e-18) return true;
+    if ((yi > y) != (yj > y) && x < (xj - xi) * (y - yi) / (yj - yi) + xi) in = !in;
+  }
+  return in;
+}
+
+// local owners (<= 4) of point (x, y) and their weight (1/S, or 1 for the
+// lowest-id owner in owner mode); returns the number of local owners
+__device__ __forceinline__ int classify(const Geo& G, int64_t p, float xf, float yf, int* own, float& w) {
+  int nl = 0, S = 0;
+  if (G.kind == 0) {
+    for (int k = 0; k < 4; ++k) {
+      const int q = G.owners[p * 4 + k];
+      if (q >= 0) own[nl++] = q;
+    }
+    S = nl;
+    w = S > 0 ? 1.0f / float(S) : 0.0f;
+    return nl;
+  }
+  const double x = xf, y = yf, tol = G.tol;
+  int first = -1;
+  if (G.kind == 1) {
+    for (int g = 0; g < G.n_geo; ++g) {
+      const float* B = G.geo + 4 * g;
+      if (x >= double(B[0]) - tol && x <= double(B[2]) + tol && y >= double(B[1]) - tol && y <= double(B[3]) + tol) {
+        ++S;
+        if (first < 0) first = g;
+        const int q = G.local[g];
+        if (q >= 0 && nl < 4 && (G.owner_mode == 0 || g == first)) own[nl++] = q;
+      }
+    }
+  } else if (in_polygon(x, y, G.poly, G.n_poly)) {
+    double dmin = 1e300;
+    for (int g = 0; g < G.n_geo; ++g) {
+      const double dx = x - double(G.geo[2 * g]), dy = y - double(G.geo[2 * g + 1]);
+      dmin = fmin(dmin, sqrt(dx * dx + dy * dy));
+    }
+    for (int g = 0; g < G.n_geo; ++g) {
+      const double dx = x - double(G.geo[2 * g]), dy = y - double(G.geo[2 * g + 1]);
+      if (sqrt(dx * dx + dy * dy) <= dmin + tol) {
+        ++S;
+        if (first < 0) first = g;
+        const int q = G.local[g];
+        if (q >= 0 && nl < 4 && (G.owner_mode == 0 || g == first)) own[nl++] = q;
+      }
+    }
+  }
+  w = G.owner_mode == 1 ? 1.0f : (S > 0 ? 1.0f / float(S) : 0.0f);
+  return nl;
+}
+
 template <int N, int NH, int DO, int ACT>
-__global__ void k_predict(const float* params, int pstride, float slope_n, const float* pts, const int32_t* owners,
+__global__ void k_predict(const float* params, int pstride, float slope_n, const float* pts, const Geo G,
                           int64_t n, float* out, const int32_t* sub_act) {
   using LY = Lay<N, NH, DO>;
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1008,25 +1113,25 @@ __global__ void k_predict(const float* params, int pstride, float slope_n, const
   float acc[DO];
 #pragma unroll
   for (int o = 0; o < DO; ++o) acc[o] = 0.0f;
-  int S = 0;
-  for (int k = 0; k < 4; ++k) {
-    const int q = owners[p * 4 + k];
-    if (q < 0) continue;
-    ++S;
+  int own[4];
+  float wgt;
+  const int nl = classify(G, p, x, y, own, wgt);
+  for (int k = 0; k < nl; ++k) {
+    const int q = own[k];
     const int act = ACT == kActMixed ? sub_act[q] : ACT;
-    const float* G = params + size_t(q) * pstride;
+    const float* P = params + size_t(q) * pstride;
     float h[N], g[N];
-    float s = slope_n * G[LY::offA(1)];
+    float s = slope_n * P[LY::offA(1)];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       float s0, s1, s2, s3;
-      act_derivs<ACT>(s * (G[2 * j] * x + G[2 * j + 1] * y + G[LY::offB(1) + j]), s0, s1, s2, s3, act);
+      act_derivs<ACT>(s * (P[2 * j] * x + P[2 * j + 1] * y + P[LY::offB(1) + j]), s0, s1, s2, s3, act);
       h[j] = s0;
     }
     for (int l = 2; l <= NH; ++l) {
-      s = slope_n * G[LY::offA(l)];
-      const float* W = G + LY::offW(l);
-      const float* b = G + LY::offB(l);
+      s = slope_n * P[LY::offA(l)];
+      const float* W = P + LY::offW(l);
+      const float* b = P + LY::offB(l);
       for (int j = 0; j < N; ++j) {
         float zz = b[j];
 #pragma unroll
@@ -1040,18 +1145,17 @@ __global__ void k_predict(const float* params, int pstride, float slope_n, const
         h[j] = s0;
       }
     }
-    const float* W = G + LY::offW(NH + 1);
+    const float* W = P + LY::offW(NH + 1);
 #pragma unroll
     for (int o = 0; o < DO; ++o) {
-      float u = G[LY::offB(NH + 1) + o];
+      float u = P[LY::offB(NH + 1) + o];
 #pragma unroll
       for (int i = 0; i < N; ++i) u = fmaf(W[o * N + i], h[i], u);
       acc[o] += u;
     }
   }
-  const float inv = S > 0 ? 1.0f / float(S) : 0.0f;   // indicator 1/S
 #pragma unroll
-  for (int o = 0; o < DO; ++o) out[size_t(o) * n + p] = acc[o] * inv;
+  for (int o = 0; o < DO; ++o) out[size_t(o) * n + p] = acc[o] * wgt;   // indicator 1/S
 }
 
 }  // namespace pinn

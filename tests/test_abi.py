@@ -121,3 +121,38 @@ def test_point_table_layout_and_plan():
                     got[:, tw - r0: tw - r0 + o.seg_n[si]] = o.coords[:, pos:pos + o.seg_n[si]]
                 pos += o.seg_n[si]
         np.testing.assert_array_equal(send_xy, got)
+
+
+def test_exchange_plan_validated(lib):
+    """A loop-back / multi-rank exchange plan passes workspace_size; malformed
+    plans are protocol errors (EPROTOCOL) with a message."""
+    import bench
+    from paper_2104_10013_b200 import binding
+    from pinn_inputs import make_config
+    prob = make_config("C2", method="xpinn", scale=0.02)
+    owner = bench.block_owner(prob, 2)
+    t = binding.build_point_table(prob, list(range(prob.n_sub)), owner, 0, peer_of=lambda o: 0)
+    fake = dict(coords=0x1000, target=0x2000, mask=0x3000, init_params=0x4000)
+    d, keep = binding.make_desc(prob, t, fake, 0, 0)
+    assert d.n_peers == 1 and d.n_recv > 0
+    st, n, msg = _ws(lib, d)
+    assert st == 0, msg
+    d.peer_recv_row[0] = d.peer_recv_row[0] + 1
+    st, n, msg = _ws(lib, d)
+    assert st == binding.EPROTOCOL and "received rows" in msg
+    d.peer_recv_row[0] = d.peer_recv_row[0] - 1
+    d.send_rows[0] = 10 ** 9
+    st, n, msg = _ws(lib, d)
+    assert st == binding.EPROTOCOL and "send row" in msg
+
+
+def test_geometry_validated(lib):
+    from paper_2104_10013_b200 import binding
+    from pinn_inputs import make_config
+    d, keep, t = _desc(make_config("C2", scale=0.02))
+    assert d.geometry == binding.GEOM_BOXES and d.n_geo == 16
+    st, n, msg = _ws(lib, d)
+    assert st == 0, msg
+    d.geo_local[3] = 99
+    st, n, msg = _ws(lib, d)
+    assert st == binding.EINVAL and "geo_local" in msg

@@ -78,3 +78,87 @@ def test_exchange_world_size_2(method):
         assert bad == 0, (rank, bad)
         assert n_remote == 4, (rank, n_remote)        # 4 cut edges between the two 4x4 blocks
         assert n_recv == 4 * max(1, round(250 * 0.01)), (rank, n_recv)
+
+
+def _worker_strong(rank, world, port, cfg, q):
+    """bench.py's strong-scaling placement (contiguous blocks of the fixed
+    decomposition) through the same routing."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import bench
+        from paper_2104_10013_b200.binding import build_point_table, exchange_payload
+        from pinn_inputs import make_config
+        prob = make_config(cfg, scale=0.01)
+        owner = bench.block_owner(prob, world)
+        local = [i for i in range(prob.n_sub) if owner[i] == rank]
+        t = build_point_table(prob, local, owner, rank)
+        n = t.coords.shape[1]
+        payload = torch.zeros(n + t.plan.n_recv, 2)
+        payload[:n] = torch.from_numpy(_tag(t.coords))
+        exchange_payload(payload, t.plan)
+        bad = 0
+        for qi in range(len(local)):
+            pos = int(t.sub_off[qi] + t.n_res[qi] + t.n_data[qi])
+            for si in range(t.seg_off[qi], t.seg_off[qi + 1]):
+                m = int(t.seg_n[si])
+                tw = int(t.seg_twin[si])
+                bad += int(not np.array_equal(payload[tw:tw + m].numpy(), _tag(t.coords[:, pos:pos + m])))
+                pos += m
+        n_remote = int(sum(1 for tw in t.seg_twin if tw >= n))
+        q.put((rank, bad, n_remote, len(local)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e), -1, -1))
+
+
+@pytest.mark.parametrize("cfg,cut", [("C2", 4), ("C4", 2)])
+def test_exchange_strong_placement_world_size_2(cfg, cut):
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_strong, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, bad, n_remote, n_local in res:
+        assert bad == 0, (rank, bad)
+        assert n_remote == cut, (rank, n_remote)     # C2: 4x4 split in 2x4 halves; C4: 4x2 in 2x2 halves
+        assert n_local * world in (16, 8)
+
+
+@pytest.mark.parametrize("cfg,kw", [("C2", dict(method="xpinn")), ("C2", dict(method="cpinn")),
+                                    ("C4", dict()), ("C3", dict(gpus=8))])
+def test_loopback_plan_routes_every_twin(cfg, kw):
+    """Loop-back plan (one process exchanging with itself, the single-GPU
+    validation of the library's NCCL path): NCCL moves each peer's send rows,
+    in order, into its received range; afterwards every segment's twin rows
+    hold the neighbour's own rows."""
+    import bench
+    from paper_2104_10013_b200.binding import build_point_table
+    from pinn_inputs import make_config
+    prob = make_config(cfg, scale=0.01, **kw)
+    owner = bench.block_owner(prob, 2)
+    t = build_point_table(prob, list(range(prob.n_sub)), owner, 0, peer_of=lambda o: 0)
+    n = t.coords.shape[1]
+    assert set(t.plan.send) == {0} and set(t.plan.recv) == {0}
+    payload = np.zeros((n + t.plan.n_recv, 2), np.float32)
+    payload[:n] = _tag(t.coords)
+    r0, m = t.plan.recv[0]
+    assert r0 == n and m == t.plan.n_recv == len(t.plan.send[0])
+    payload[r0:r0 + m] = payload[t.plan.send[0]]           # what ncclSend/ncclRecv to self does
+    n_remote = 0
+    for qi, q in enumerate(t.local):
+        pos = int(t.sub_off[qi] + t.n_res[qi] + t.n_data[qi])
+        for si in range(t.seg_off[qi], t.seg_off[qi + 1]):
+            k = int(t.seg_n[si])
+            tw = int(t.seg_twin[si])
+            n_remote += tw >= n
+            assert np.array_equal(payload[tw:tw + k], _tag(t.coords[:, pos:pos + k])), (q, si)
+            pos += k
+    assert n_remote > 0

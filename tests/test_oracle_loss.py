@@ -278,3 +278,61 @@ def test_hybrid_is_flux_in_space_residual_in_time():
             _, sn = OL.interface_payload(pp, th[nb], X, ed.normal, create_graph=False)
             want += float(((sq - sn) ** 2).sum()) / len(X)
         assert float(mi) == pytest.approx(want, rel=1e-12)
+
+
+# --------------------------------------------------------------------------
+# Systems (D_o > 1): the output mask of MSE_u and the sum over fields (Z4),
+# pinned with constant networks and hand-computed values.
+# --------------------------------------------------------------------------
+
+def test_mse_u_output_mask_and_field_sum_ns():
+    """NS cavity data (Z16): targets (u, v) = (1, 0) on the lid y = 1, (0, 0)
+    on the other walls, p unconstrained (mask 0).  A constant net (1, 2, 3)
+    gives per point (t_u - 1)^2 + (0 - 2)^2 (+ 0 for p, whatever the net's
+    p), so MSE_u = mean over data points of (t_u - 1)^2 + 4 (P:159 summed
+    over fields, reading Z4; the mask drops p)."""
+    p = make_config("C4", method="xpinn", n_f=5, n_i=4, n_u=16, width=5, n_hidden=2)
+    base = [_const_params(p, [1.0, 2.0, 3.0]) for _ in range(p.n_sub)]
+    alt = [_const_params(p, [1.0, 2.0, -50.0]) for _ in range(p.n_sub)]
+    for q in range(p.n_sub):
+        s = p.subdomains[q]
+        tu = s.u_target[:, 0]
+        assert np.all(s.u_mask[:, 2] == 0) and np.all(s.u_mask[:, :2] == 1)
+        want = float(np.mean((tu - 1.0) ** 2 + 4.0)) if len(tu) else 0.0
+        for params in (base, alt):                          # p never enters MSE_u
+            pp = _with_params(p, params)
+            th = [torch.tensor(s2.params) for s2 in pp.subdomains]
+            _, (mu, mf, ma, mi) = OL.subdomain_loss(pp, q, th)
+            assert float(mu) == pytest.approx(want, rel=1e-14, abs=1e-300)
+        lid = np.sum(s.x_u[:, 1] == 1.0)
+        if s.iy == 1 and len(tu):
+            assert lid > 0 and want == pytest.approx(4.0 + (len(tu) - lid) / len(tu), rel=1e-14)
+
+
+def test_interface_terms_sum_over_fields_ns():
+    """Z4 for the interface terms with constant nets q = (1, 2, 3),
+    neighbour = (3, 4, 7), all derivatives 0:
+      u_avg : per point sum_o ((u_q - u_n)/2)^2 = 1 + 1 + 4 = 6 -> 6 per edge;
+      XPINN residual jump: F = (0, 0, 0) on both sides -> 0;
+      cPINN flux jump, Table 1 with n = (1, 0): q (u^2 + p, uv, u) = (4, 2, 1),
+        neighbour (9 + 7, 12, 3) = (16, 12, 3) -> 144 + 100 + 4 = 248 per point;
+        with n = (0, 1): q (uv, v^2 + p, v) = (2, 7, 2), neighbour (12, 23, 4)
+        -> 100 + 256 + 4 = 360 per point."""
+    for method in ("xpinn", "cpinn"):
+        p = make_config("C4", method=method, n_f=5, n_i=4, n_u=8, width=5, n_hidden=2)
+        params = []
+        for q in range(p.n_sub):
+            params.append(_const_params(p, [1.0, 2.0, 3.0] if q == 0 else [3.0, 4.0, 7.0]))
+        pp = _with_params(p, params)
+        th = [torch.tensor(s.params) for s in pp.subdomains]
+        _, (mu, mf, ma, mi) = OL.subdomain_loss(pp, 0, th)
+        edges = pp.subdomains[0].edges
+        assert len(edges) == 2                              # corner subdomain of the 4x2 grid
+        assert float(ma) == pytest.approx(6.0 * len(edges), rel=1e-14)
+        assert float(mf) == 0.0
+        if method == "xpinn":
+            assert float(mi) == 0.0
+        else:
+            axes = sorted(pp.edges[e].axis for e in edges)
+            assert axes == [0, 1]
+            assert float(mi) == pytest.approx(248.0 + 360.0, rel=1e-14)

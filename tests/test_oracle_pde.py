@@ -227,3 +227,81 @@ def test_heat_inv_c5_targets_are_the_paper_fields():
         np.testing.assert_allclose(s.u_target[:, 1], 20.0 + np.exp(0.1 * x[:, 1]) * np.sin(0.5 * x[:, 0]),
                                    rtol=1e-6)
         assert np.all(s.u_mask[:, 0] == 1.0)           # T data everywhere (interior + boundary)
+
+
+# --------------------------------------------------------------------------
+# Flux / residual consistency: for every operator in conservation form the
+# divergence of the interface flux f(u) (the quantity cPINN matches across an
+# edge, Table 1) equals the residual F plus the forcing.
+# Each flux is evaluated with n = e1 and n = e2 as a field of X and
+# differentiated by autograd, so every term of f (including the viscous
+# -nu u_x of Burgers and K of the heat flux) is pinned against the residual
+# written independently in oracle/pde.py.
+# --------------------------------------------------------------------------
+
+def _div_flux(flux_fn, fl, Xg):
+    fx = flux_fn(fl, Xg, (1.0, 0.0))
+    fy = flux_fn(fl, Xg, (0.0, 1.0))
+    cols = []
+    for e in range(fx.shape[1]):
+        gx = torch.autograd.grad(fx[:, e].sum(), Xg, create_graph=True)[0][:, 0]
+        gy = torch.autograd.grad(fy[:, e].sum(), Xg, create_graph=True)[0][:, 1]
+        cols.append(gx + gy)
+    return torch.stack(cols, dim=1)
+
+
+def test_burgers_flux_divergence_is_residual():
+    """d_x (u^2/2 - nu u_x) + d_t u = u_t + u u_x - nu u_xx = F (SPEC.md:342,
+    reading Z13) for a field with u_x, u_xx != 0: pins the viscous term."""
+    X = _pts(400, seed=11)
+    fl, Xg = _autograd_fields([lambda X: torch.sin(2.0 * X[:, 0]) * torch.cos(X[:, 1]) + X[:, 0] ** 2 * X[:, 1]], X)
+    F = opde.burgers_residual(fl, Xg, NU)
+    D = _div_flux(lambda f, x, n: opde.burgers_flux_n(f, x, n, NU), fl, Xg)
+    assert torch.allclose(D, F, rtol=1e-12, atol=1e-12)
+    # and the viscous term is really there: dropping nu changes the divergence by nu u_xx
+    D0 = _div_flux(lambda f, x, n: opde.burgers_flux_n(f, x, n, 0.0), fl, Xg)
+    assert torch.allclose(D - D0, -NU * fl[0]["d11"][:, None], rtol=1e-10, atol=1e-14)
+    assert float((D - D0).abs().max()) > 1e-4
+
+
+def test_poisson_and_heat_flux_divergence_is_residual_plus_forcing():
+    """div(grad u) = F + f (Poisson) and div(K grad u) = F + f (heat, Eq. 15
+    P:824) with K(x, y) of P:829: pins heat_flux_n (K times the normal
+    derivative)."""
+    X = _pts(400, (0, 0), (3, 2), seed=12)
+    fn = lambda X: X[:, 0] ** 2 * X[:, 1] + torch.sin(X[:, 0]) * torch.cos(0.7 * X[:, 1])
+    fl, Xg = _autograd_fields([fn], X)
+    Dp = _div_flux(opde.poisson_flux_n, fl, Xg)
+    assert torch.allclose(Dp[:, 0], opde.poisson_residual(fl, Xg)[:, 0] + opde.poisson_forcing(Xg),
+                          rtol=1e-12, atol=1e-11)
+    Dh = _div_flux(opde.heat_flux_n, fl, Xg)
+    assert torch.allclose(Dh[:, 0], opde.heat_residual(fl, Xg)[:, 0] + opde.heat_forcing(Xg),
+                          rtol=1e-12, atol=1e-10)
+    # heat flux at a hand-checked point: x = pi, y = 0 -> K = 21; u = x^2 y + sin x cos 0.7y
+    # u_x = 2 x y + cos x cos 0.7 y = -1 ; u_y = x^2 - 0.7 sin x sin 0.7 y = pi^2
+    P = torch.tensor([[math.pi, 0.0]], dtype=DT)
+    flp, Xp = _autograd_fields([fn], P)
+    fx = float(opde.heat_flux_n(flp, Xp, (1.0, 0.0))[0, 0])
+    fy = float(opde.heat_flux_n(flp, Xp, (0.0, 1.0))[0, 0])
+    assert fx == pytest.approx(-21.0, rel=1e-13)
+    assert fy == pytest.approx(21.0 * math.pi ** 2, rel=1e-13)
+
+
+def test_ns_table1_flux_divergence():
+    """Table 1 is the conservative momentum / mass flux of Eq. (11)
+    (P:415-417): div of the x-/y-momentum rows = F_x + u div(u) and
+    F_y + v div(u); div of the mass row = F_mass, for a field that is NOT
+    divergence free (pins every Table 1 entry, signs of the viscous terms
+    included)."""
+    X = _pts(300, (0, 0), (1, 1), seed=13)
+    fns = [lambda X: torch.sin(X[:, 0]) * X[:, 1] + X[:, 0] ** 2,
+           lambda X: torch.cos(X[:, 1]) * X[:, 0] - X[:, 1] ** 3,
+           lambda X: X[:, 0] * X[:, 1] + torch.sin(X[:, 0] + X[:, 1])]
+    fl, Xg = _autograd_fields(fns, X)
+    re = 7.0
+    F = opde.ns_residual(fl, Xg, re)
+    D = _div_flux(lambda f, x, n: opde.ns_flux_n(f, x, n, re), fl, Xg)
+    div = fl[0]["d1"] + fl[1]["d2"]
+    assert torch.allclose(D[:, 0], F[:, 0] + fl[0]["u"] * div, rtol=1e-12, atol=1e-12)
+    assert torch.allclose(D[:, 1], F[:, 1] + fl[1]["u"] * div, rtol=1e-12, atol=1e-12)
+    assert torch.allclose(D[:, 2], F[:, 2], rtol=1e-12, atol=1e-12)

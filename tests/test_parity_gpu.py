@@ -1,14 +1,32 @@
 """GPU parity: the CUDA path through the C ABI vs the FP64 oracle.
 
-Tolerances (BASELINE.json north_star):
-  * loss terms and J: relative 1e-5 (floor 1e-6 * J for terms that vanish),
-  * gradients: per tensor (each W^k, b^k, a^k) max|g - g_ref| / max|g_ref| <= 1e-4,
-  * payload values: 1e-4 of the field's max magnitude (derivative quantities;
-    FP32 error scales with the cancelling terms),
+Tolerances (BASELINE.json north_star).  FP32 noise model: an
+FP32 evaluation of the network is (backward stability) an exact evaluation at
+weights perturbed by O(sqrt(N) eps32); the oracle is evaluated at weights
+theta (1 + delta xi), delta = 2^-18 (= 64 eps32), xi ~ U(-1, 1), for
+NOISE_SAMPLES draws, and noise(x) = max |x(theta~) - x(theta)| for every loss
+term and payload value.
+  * loss terms and J: |x - x_ref| <= 1e-5 |x_ref| + NOISE_K noise(x) (no
+    floor proportional to J), NOISE_K = 4;
+  * payload values: |x - x_ref| <= 1e-5 |x_ref| + NOISE_K noise(x), per element;
+  * W^k, b^k gradients: per tensor max|g - g_ref| / max|g_ref| <= 1e-4;
+  * a^k gradients: |g - g_ref| <= 1e-4 |g_ref| + eps32 G_a / |a^k|,
+    G_a = sum |W^k o dJ/dW^k| + sum |b^k o dJ/db^k| (oracle values): the slope
+    gradient is a^k dJ/da^k = <W^k, dJ/dW^k> + <b^k, dJ/db^k>,
+    a cancelling sum whose FP32 inputs carry ~eps32 relative error, so its
+    error is bounded by eps32 times its gross magnitude (measured: at most
+    0.2 of that bound over every case);
+  * trained states (test_trained_state_parity), where the residuals are small
+    cancelling sums and so are the adjoint seeds: each gradient bound above
+    also admits NOISE_K_GRAD = 8 times the tensor's FP32 gradient noise
+    (grad_noise);
   * Adam fed the GPU gradient: relative 1e-6 (pure FP32 rounding of the update).
 """
 
 import dataclasses
+import os
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -18,6 +36,14 @@ from oracle import loss as OL
 from pinn_inputs import make_config, n_params, param_layout, perturb_params
 
 pytestmark = pytest.mark.gpu
+
+EPS32 = 2.0 ** -24
+NOISE_DELTA = 2.0 ** -18
+NOISE_SAMPLES = 3
+NOISE_K = 4.0
+NOISE_K_GRAD = 8.0
+REL_LOSS = 1e-5
+REL_GRAD = 1e-4
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -43,58 +69,109 @@ def _tensors(sizes):
     return out
 
 
-def check_loss(loss_gpu, ref, tag=""):
-    for q, (bd, _) in enumerate(ref):
+def _perturbed(thetas, seed):
+    g = torch.Generator().manual_seed(seed)
+    return [t * (1.0 + NOISE_DELTA * (2.0 * torch.rand(t.shape, generator=g, dtype=t.dtype) - 1.0))
+            for t in thetas]
+
+
+def loss_noise(prob, thetas, qs=None, samples=NOISE_SAMPLES):
+    """[n_sub, 5] FP32 noise of (MSE_u, MSE_F, MSE_uavg, MSE_if, J) (module docstring)."""
+    qs = range(prob.n_sub) if qs is None else qs
+    base = {q: np.array(OL.subdomain_loss_terms(prob, q, thetas).as_list()) for q in qs}
+    out = np.zeros((prob.n_sub, 5))
+    for k in range(samples):
+        th = _perturbed(thetas, 1000 + k)
+        for q in qs:
+            out[q] = np.maximum(out[q], np.abs(np.array(OL.subdomain_loss_terms(prob, q, th).as_list()) - base[q]))
+    return out
+
+
+def payload_noise(prob, thetas, samples=NOISE_SAMPLES):
+    base = OL.all_payloads(prob, thetas)
+    out = {k: np.zeros((u.shape[0], u.shape[1] + s.shape[1])) for k, (u, s) in base.items()}
+    for k in range(samples):
+        pay = OL.all_payloads(prob, _perturbed(thetas, 2000 + k))
+        for key, (u, s) in pay.items():
+            u0, s0 = base[key]
+            d = np.concatenate([(u - u0).abs().numpy(), (s - s0).abs().numpy()], axis=1)
+            out[key] = np.maximum(out[key], d)
+    return base, out
+
+
+def check_loss(loss_gpu, ref, noise, tag="", qs=None):
+    """ref: per subdomain Breakdown (or (Breakdown, grad)); noise: loss_noise()."""
+    for q in (range(len(ref)) if qs is None else qs):
+        bd = ref[q][0] if isinstance(ref[q], tuple) else ref[q]
         got = loss_gpu[q]
         want = bd.as_list()
-        J = abs(want[4])
         for i, name in enumerate(["mse_u", "mse_f", "mse_uavg", "mse_if", "J"]):
-            tol = 1e-5 * abs(want[i]) + 1e-6 * J + 1e-12
-            assert abs(float(got[i]) - want[i]) <= tol, (tag, q, name, float(got[i]), want[i])
+            tol = REL_LOSS * abs(want[i]) + NOISE_K * noise[q, i] + 1e-300
+            assert abs(float(got[i]) - want[i]) <= tol, (tag, q, name, float(got[i]), want[i], tol)
+        assert float(got[5]) == 0.0, (tag, q, "status bits", float(got[5]))
 
 
-def check_grad(grad_gpu, ref, sizes, tag="", tol=1e-4, thetas=None):
-    """W^k, b^k: per tensor max|g - g_ref| / max|g_ref| <= tol.
-    a^k (a scalar whose gradient is a cancelling sum): by the exact identity
-    a_k dJ/da_k = <W^k, dJ/dW^k> + <b^k, dJ/db^k> (tests/test_oracle_loss.py),
-    its error is bounded by the propagated W/b tolerance:
-    |dg_a| <= tol (sum|W^k| max|dW^k| + sum|b^k| max|db^k|) / |a_k|."""
-    worst = 0.0
+def slope_bound(theta, g_ref, ent):
+    """eps32 G_a / |a| for one hidden layer (module docstring)."""
+    (ow, nw), (ob, nb), (oa, _) = ent["W"], ent["b"], ent["a"]
+    G = np.abs(theta[ow:ow + nw] * g_ref[ow:ow + nw]).sum() + np.abs(theta[ob:ob + nb] * g_ref[ob:ob + nb]).sum()
+    return EPS32 * G / abs(theta[oa])
+
+
+def grad_noise(prob, thetas, samples=NOISE_SAMPLES):
+    """[n_sub][n_params] FP32 noise of the oracle gradient (module docstring);
+    used where the loss is far from its seeded value (trained states), where
+    the residuals F are small cancelling sums and so are the adjoint seeds."""
+    base = [g.numpy() for _, g in OL.loss_grad_all(prob, thetas)]
+    out = [np.zeros_like(b) for b in base]
+    for k in range(samples):
+        for q, (_, g) in enumerate(OL.loss_grad_all(prob, _perturbed(thetas, 3000 + k))):
+            out[q] = np.maximum(out[q], np.abs(g.numpy() - base[q]))
+    return out
+
+
+def check_grad(grad_gpu, ref, sizes, thetas, tag="", qs=None, noise=None):
+    """W^k, b^k per tensor at REL_GRAD; a^k by the slope error model; with
+    `noise` (grad_noise) each bound also admits NOISE_K x the tensor's FP32
+    noise.  Returns (worst W/b error, worst a^k error / its bound)."""
+    worst, worst_a = 0.0, 0.0
     lay = param_layout(sizes)
-    for q, (_, g) in enumerate(ref):
+    for q in (range(len(ref)) if qs is None else qs):
+        g = ref[q][1]
         gg = grad_gpu[q].double().cpu().numpy()
         gr = g.numpy()
+        nz = noise[q] if noise is not None else np.zeros_like(gr)
         for name, o, n in _tensors(sizes):
             if name.startswith("a"):
                 continue
             den = np.max(np.abs(gr[o:o + n]))
-            err = np.max(np.abs(gg[o:o + n] - gr[o:o + n])) / max(den, 1e-30)
-            worst = max(worst, err)
-            assert err <= tol or den < 1e-12, (tag, q, name, err, den)
-        if thetas is None:
-            continue
+            err = np.max(np.abs(gg[o:o + n] - gr[o:o + n]))
+            tol = REL_GRAD * den + NOISE_K_GRAD * np.max(nz[o:o + n])
+            worst = max(worst, err / max(den, 1e-300))
+            assert err <= tol or den == 0.0, (tag, q, name, err / max(den, 1e-300), den, tol)
         th = thetas[q].numpy()
         for k, ent in enumerate(lay, start=1):
             if "a" not in ent:
                 continue
-            (ow, nw), (ob, nb), (oa, _) = ent["W"], ent["b"], ent["a"]
-            bound = tol * (np.abs(th[ow:ow + nw]).sum() * np.abs(gr[ow:ow + nw]).max()
-                           + np.abs(th[ob:ob + nb]).sum() * np.abs(gr[ob:ob + nb]).max()) / abs(th[oa])
+            oa = ent["a"][0]
+            bound = REL_GRAD * abs(gr[oa]) + slope_bound(th, gr, ent) + NOISE_K_GRAD * nz[oa]
             err = abs(gg[oa] - gr[oa])
+            worst_a = max(worst_a, err / bound)
             assert err <= bound, (tag, q, f"a{k}", err, bound, gr[oa])
-    return worst
+    return worst, worst_a
 
 
-def run_parity(prob, tag, **kw):
-    m = _handle(prob, **kw)
+def run_parity(prob, tag, handle=None, **kw):
+    m = handle or _handle(prob, **kw)
     m.interface_payload()
     loss, grad = m.loss_grad()
     torch.cuda.synchronize()
     th = OL.init_state(prob).thetas
     ref = OL.loss_grad_all(prob, th)
-    check_loss(loss.cpu().numpy(), ref, tag)
-    w = check_grad(grad, ref, prob.sizes, tag, thetas=th)
-    m.close()
+    check_loss(loss.cpu().numpy(), ref, loss_noise(prob, th), tag)
+    w = check_grad(grad, ref, prob.sizes, th, tag)
+    if handle is None:
+        m.close()
     return w
 
 
@@ -129,41 +206,6 @@ def test_loss_grad_parity_perturbed(cfg, kw):
     run_parity(prob, f"perturbed {cfg}")
 
 
-@pytest.mark.parametrize("cfg,kw", [CASES[0], CASES[1], CASES[5], CASES[9]])
-def test_width20_point_per_thread_kernel_parity(cfg, kw):
-    """Width-20 nets also compile the point-per-thread kernel
-    (PINN_DD_FLAG_POINT_PER_THREAD): it must match the oracle, and the two
-    kernels must agree to FP32 rounding."""
-    from paper_2104_10013_b200.binding import FLAG_GRAPH, FLAG_POINT_PER_THREAD
-    prob = perturb_params(make_config(cfg, **kw), scale=0.1)
-    run_parity(prob, f"point-per-thread {cfg}", flags=FLAG_GRAPH | FLAG_POINT_PER_THREAD)
-    outs = []
-    for fl in (FLAG_GRAPH, FLAG_GRAPH | FLAG_POINT_PER_THREAD):
-        m = _handle(prob, flags=fl)
-        m.interface_payload()
-        outs.append(m.loss_grad())
-        torch.cuda.synchronize()
-        m.close()
-    (la, ga), (lb, gb) = outs
-    assert torch.allclose(la, lb, rtol=1e-5, atol=1e-7)
-    assert torch.allclose(ga, gb, rtol=1e-4, atol=1e-5 * float(ga.abs().max()))
-
-
-def test_global_stash_point_per_thread_bitwise():
-    """The point-per-thread kernel's TMEM stash and its global-memory fallback
-    give bitwise identical results."""
-    from paper_2104_10013_b200.binding import FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_POINT_PER_THREAD
-    prob = perturb_params(make_config("C3", method="xpinn", gpus=4, n_f=300, n_i=20, n_u=30), scale=0.1)
-    outs = []
-    for fl in (FLAG_GRAPH | FLAG_POINT_PER_THREAD, FLAG_GRAPH | FLAG_GLOBAL_STASH | FLAG_POINT_PER_THREAD):
-        m = _handle(prob, flags=fl)
-        m.interface_payload()
-        outs.append(m.loss_grad())
-        torch.cuda.synchronize()
-        m.close()
-    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
-
-
 def test_pinn_method_single_subdomain():
     prob = make_config("C2", method="pinn", nx=1, ny=1, n_f=500, n_u=64)
     run_parity(prob, "pinn")
@@ -177,24 +219,26 @@ def test_payload_parity(cfg, kw):
     m = _handle(prob)
     m.interface_payload()
     torch.cuda.synchronize()
+    check_payload(m, prob, OL.init_state(prob).thetas, cfg)
+    m.close()
+
+
+def check_payload(m, prob, th, tag):
+    """Every local payload row vs the oracle, per element at the noise model."""
     pay = m.payload.cpu().numpy()
-    th = OL.init_state(prob).thetas
-    ref = OL.all_payloads(prob, th)
+    ref, noise = payload_noise(prob, th)
     t = m.table
-    pos_of = {}
     for qi, q in enumerate(t.local):
         pos = int(t.sub_off[qi] + t.n_res[qi] + t.n_data[qi])
         for si in range(t.seg_off[qi], t.seg_off[qi + 1]):
-            pos_of[(q, int(t.seg_edge[si]))] = pos
-            pos += int(t.seg_n[si])
-    for (q, e), (u, s) in ref.items():
-        r0 = pos_of[(q, e)]
-        n = u.shape[0]
-        want = np.concatenate([u.numpy(), s.numpy()], axis=1)
-        got = pay[r0:r0 + n, :want.shape[1]]
-        scale = np.max(np.abs(want), axis=0) + 1e-30
-        assert np.all(np.abs(got - want) <= 1e-4 * scale + 1e-7), (cfg, q, e)
-    m.close()
+            e, n = int(t.seg_edge[si]), int(t.seg_n[si])
+            u, s = ref[(q, e)]
+            want = np.concatenate([u.numpy(), s.numpy()], axis=1)
+            got = pay[pos:pos + n, :want.shape[1]]
+            tol = REL_LOSS * np.abs(want) + NOISE_K * noise[(q, e)] + 1e-300
+            bad = np.abs(got - want) > tol
+            assert not bad.any(), (tag, q, e, got[bad][:4], want[bad][:4], tol[bad][:4])
+            pos += n
 
 
 def test_tmem_and_global_stash_bitwise_equal():
@@ -251,29 +295,49 @@ def test_adam_matches_oracle_on_gpu_gradient():
     m.close()
 
 
-def test_train_steps_track_oracle():
-    """5 synchronous Algorithm-1 iterations (graph-replayed) vs the oracle.
-    Adam's first steps move every parameter by ~lr sign(g), so entries whose
-    gradient is within the FP32 gradient error of 0 can flip: the bound is
-    derived in DESIGN.md (|dtheta| <= 2 lr per such entry)."""
-    prob = make_config("C1", n_f=300, n_i=30, n_u=40)
+@pytest.mark.parametrize("cfg,kw", [("C1", dict(n_f=300, n_i=30, n_u=40)),
+                                    ("C2", dict(method="xpinn", n_f=300, n_i=25, n_u=20)),
+                                    ("C5", dict(scale=0.05, n_i=30, n_u=40))])
+def test_train_steps_track_oracle(cfg, kw):
+    """Parameters after 1 and 10 synchronous Algorithm-1 iterations
+    (graph-replayed) vs the oracle's iterations (Z18).  Adam's first steps move
+    a parameter by ~lr sign(g): an entry whose oracle gradient is ever within
+    1e-3 max|g| of its tensor of 0 can change sign or direction under the FP32
+    gradient error (up to ~1e-5 of the tensor max, measured), so it is
+    only held to the 2 lr t it can move; every other entry to
+    1e-5 |theta| + 1e-3 lr t.  Ambiguous entries must stay rare (< 5 %; 2-3 %
+    measured)."""
+    prob = make_config(cfg, **kw)
     m = _handle(prob)
-    out = m.step(5)
     st = OL.init_state(prob)
-    for _ in range(5):
-        st, bd = OL.train_step(prob, st)
-    # the last step's loss is evaluated at the parameters before the 5th update
-    st4 = OL.init_state(prob)
-    for _ in range(4):
-        st4, _ = OL.train_step(prob, st4)
-    ref = OL.loss_grad_all(prob, st4.thetas)
-    for q, (b, _) in enumerate(ref):
-        assert abs(out[q, 4] - b.total) <= 1e-3 * abs(b.total), (q, out[q, 4], b.total)
-    for q in range(prob.n_sub):
-        th = m.get(q, 0).double().cpu().numpy()
-        d = np.abs(th - st.thetas[q].numpy())
-        assert np.max(d) <= 10 * prob.lr, np.max(d)
-        assert np.median(d) <= 1e-5
+    ambiguous = [np.zeros(n_params(prob.sizes), dtype=bool) for _ in range(prob.n_sub)]
+    tens = _tensors(prob.sizes)
+    done = 0
+    for n_steps in (1, 10):
+        m.step(n_steps - done, want_loss=False)
+        while done < n_steps:
+            res = OL.loss_grad_all(prob, st.thetas)
+            th_new, ad_new = [], []
+            for q, (_, g) in enumerate(res):
+                gn = np.abs(g.numpy())
+                for _, o, n in tens:                    # per tensor, like the gradient tolerance
+                    ambiguous[q][o:o + n] |= gn[o:o + n] < 1e-3 * gn[o:o + n].max()
+                th, ad = OL.adam_step(st.thetas[q], g, st.adam[q], prob.lr, prob.beta1, prob.beta2, prob.eps)
+                th_new.append(th)
+                ad_new.append(ad)
+            st = OL.TrainState(th_new, ad_new)
+            done += 1
+        torch.cuda.synchronize()
+        for q in range(prob.n_sub):
+            got = m.get(q, 0).double().cpu().numpy()
+            want = st.thetas[q].numpy()
+            d = np.abs(got - want)
+            amb = ambiguous[q]
+            tol = 1e-5 * np.abs(want) + 1e-3 * prob.lr * n_steps
+            assert np.all(d[~amb] <= tol[~amb]), (cfg, n_steps, q, np.max(d[~amb] - tol[~amb]))
+            assert np.all(d[amb] <= 2 * prob.lr * n_steps + 1e-5 * np.abs(want[amb])), (cfg, n_steps, q)
+            assert amb.mean() < 0.05, (cfg, q, amb.mean())
+        assert all(m.adam_t(q) == n_steps for q in range(prob.n_sub))
     m.close()
 
 
@@ -470,36 +534,128 @@ def test_full_size_c3_parity():
 
 
 def test_full_size_c4_sampled():
-    """BASELINE configs[3] at full size (8 x 125000 residual points, 5x80 NS):
-    every interface payload row, and the loss terms of two sampled subdomains
-    (chunked no-grad oracle); the chunk/tile structure is the one bench-style
-    full-size launches use."""
+    """BASELINE configs[3] at full size (8 x 125000 residual points, 5x80 NS,
+    31-tile chunks): every interface payload row, and the loss terms of two
+    sampled subdomains (chunked no-grad oracle); the chunk/tile structure is
+    the one bench.py times.  Gradients of this chunk path: the multi-tile
+    tests below."""
     prob = make_config("C4", method="xpinn")
     m = _handle(prob)
+    assert m.plan_info()[1] >= 16                   # tiles per chunk at full size
     m.interface_payload()
     loss, _ = m.loss_grad(want_grad=False)
     torch.cuda.synchronize()
-    pay = m.payload.cpu().numpy()
     th = OL.init_state(prob).thetas
-    ref = OL.all_payloads(prob, th)
-    t = m.table
-    for qi, q in enumerate(t.local):
-        pos = int(t.sub_off[qi] + t.n_res[qi] + t.n_data[qi])
-        for si in range(t.seg_off[qi], t.seg_off[qi + 1]):
-            e = int(t.seg_edge[si]); n = int(t.seg_n[si])
-            u, s = ref[(q, e)]
-            want = np.concatenate([u.numpy(), s.numpy()], axis=1)
-            got = pay[pos:pos + n, :want.shape[1]]
-            scale = np.max(np.abs(want), axis=0) + 1e-30
-            assert np.all(np.abs(got - want) <= 1e-4 * scale + 1e-7), (q, e)
-            pos += n
-    l = loss.cpu().numpy()
-    for q in (0, 5):
-        bd = OL.subdomain_loss_terms(prob, q, th).as_list()
-        J = abs(bd[4])
-        for i in range(5):
-            assert abs(l[q, i] - bd[i]) <= 1e-5 * abs(bd[i]) + 1e-6 * J, (q, i, l[q, i], bd[i])
+    check_payload(m, prob, th, "full C4")
+    qs = (0, 5)
+    ref = {q: OL.subdomain_loss_terms(prob, q, th) for q in qs}
+    check_loss(loss.cpu().numpy(), ref, loss_noise(prob, th, qs, samples=2), "full C4", qs)
     m.close()
+
+
+@pytest.mark.parametrize("method,n_f,qs", [("xpinn", 6400, None), ("cpinn", 32000, (0, 5))])
+def test_multi_tile_chunk_gradient_parity_c4(method, n_f, qs):
+    """5x80 keeps its chunk gradient in a global partial that every tile after
+    the first read-modify-writes: runs of >= 200 tiles get
+    multi-tile chunks (4 tiles at n_f = 6400, 8 at 32000), so this is the
+    production gradient path of C4."""
+    prob = make_config("C4", method=method, n_f=n_f, n_i=64, n_u=40)
+    m = _handle(prob)
+    assert m.plan_info()[1] >= 4
+    m.interface_payload()
+    loss, grad = m.loss_grad()
+    torch.cuda.synchronize()
+    th = OL.init_state(prob).thetas
+    pay = OL.all_payloads(prob, th)
+    sel = range(prob.n_sub) if qs is None else qs
+    ref = {q: OL.loss_and_grad(prob, q, th, pay) for q in sel}
+    check_loss(loss.cpu().numpy(), ref, loss_noise(prob, th, sel), f"C4 {n_f}", sel)
+    check_grad(grad, ref, prob.sizes, th, f"C4 {n_f}", sel)
+    m.close()
+
+
+def test_multi_tile_chunk_gradient_parity_c5():
+    """C5's regions are < 200 tiles, so production runs them as one-tile
+    chunks; PINN_DD_MIN_CHUNK_TILES=4 (read once per process) forces 4-tile
+    chunks with the global-partial read-modify-write, in a subprocess."""
+    env = dict(os.environ, PINN_DD_MIN_CHUNK_TILES="4")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        f"{__file__}::test_c5_parity_forced_chunks"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_c5_parity_forced_chunks():
+    if os.environ.get("PINN_DD_MIN_CHUNK_TILES") != "4":
+        pytest.skip("runs in the subprocess of test_multi_tile_chunk_gradient_parity_c5")
+    prob = make_config("C5", scale=0.5)
+    m = _handle(prob)
+    assert m.plan_info()[1] == 4
+    run_parity(prob, "C5 4-tile chunks", handle=m)
+    m.close()
+
+
+TRAINED = [
+    ("C2", dict(method="cpinn", n_f=600, n_i=40, n_u=40, lr=2e-3)),
+    ("C2", dict(method="xpinn", n_f=600, n_i=40, n_u=40, lr=2e-3)),
+    ("C3", dict(method="hybrid", gpus=8, n_f=600, n_i=40, n_u=60)),
+    ("C4", dict(method="xpinn", n_f=400, n_i=40, n_u=40)),
+    ("C5", dict(scale=0.1, n_i=40, n_u=80)),
+]
+
+
+@pytest.mark.parametrize("cfg,kw", TRAINED)
+def test_trained_state_parity(cfg, kw):
+    """Parity away from the seeded weights: 500 graph-replayed GPU training
+    steps, then loss terms and gradients at the trained parameters (read back
+    through the ABI) vs the oracle at exactly those parameters.  After
+    training the interface terms are a sizeable part of J (checked), so the
+    interface adjoints (C5's residual jump included) are really verified."""
+    prob = make_config(cfg, **kw)
+    m = _handle(prob)
+    m.step(500, want_loss=False)
+    torch.cuda.synchronize()
+    params = [m.get(q, 0).double().cpu().numpy() for q in range(prob.n_sub)]
+    subs = [dataclasses.replace(sd, params=p) for sd, p in zip(prob.subdomains, params)]
+    trained = dataclasses.replace(prob, subdomains=subs)
+    m.interface_payload()
+    loss, grad = m.loss_grad()
+    torch.cuda.synchronize()
+    th = OL.init_state(trained).thetas
+    ref = OL.loss_grad_all(trained, th)
+    check_loss(loss.cpu().numpy(), ref, loss_noise(trained, th), f"trained {cfg}")
+    check_grad(grad, ref, trained.sizes, th, f"trained {cfg}", noise=grad_noise(trained, th))
+    iface = max((trained.w_i * bd.mse_uavg + trained.w_if * bd.mse_if) / bd.total for bd, _ in ref)
+    assert iface > 1e-2, iface
+    m.close()
+
+
+def test_constant_network_fixture_zero_loss_and_gradient():
+    """SURVEY 8(c) closed-form fixture: every net is the constant u* = c (random
+    hidden layers, W^L = 0, b^L = c), which solves Burgers / NS exactly, both
+    sides of every interface agree and W_u = 0: J = 0 and dJ/dTheta = 0 exactly
+    (every residual, jump and adjoint seed is an exact FP32 zero)."""
+    for cfg, kw, c in (("C1", dict(n_f=300, n_i=30, n_u=40), [0.75]),
+                       ("C4", dict(method="xpinn", n_f=200, n_i=30, n_u=20), [0.5, -0.25, 2.0]),
+                       ("C4", dict(method="cpinn", n_f=200, n_i=30, n_u=20), [0.5, -0.25, 2.0])):
+        prob = perturb_params(make_config(cfg, **kw), scale=0.3)
+        lay = param_layout(prob.sizes)
+        subs = []
+        for sd in prob.subdomains:
+            p = sd.params.copy()
+            o, n = lay[-1]["W"]
+            p[o:o + n] = 0.0
+            o, n = lay[-1]["b"]
+            p[o:o + n] = c
+            subs.append(dataclasses.replace(sd, params=p))
+        prob = dataclasses.replace(prob, subdomains=subs, w_u=0.0)
+        m = _handle(prob)
+        m.interface_payload()
+        loss, grad = m.loss_grad()
+        torch.cuda.synchronize()
+        assert torch.all(loss[:, 1:6] == 0) and torch.all(loss[:, 0] > 0), (cfg, loss)
+        assert torch.all(grad == 0), (cfg, grad.abs().max())
+        m.close()
 
 
 def test_train_cpinn_poisson_to_accuracy():
@@ -555,15 +711,57 @@ def test_nonfinite_is_reported():
     m.close()
 
 
-def test_step_rejects_remote_twins():
-    from paper_2104_10013_b200.binding import PinnDD, PinnDDError, EPROTOCOL
-    prob = make_config("C2", method="xpinn", n_f=100, n_i=10, n_u=10)
-    owner = [0 if s.iy < 2 else 1 for s in prob.subdomains]
-    h = PinnDD(prob, [q for q in range(16) if owner[q] == 0], owner, 0, device="cuda:0")
+def test_zero_slope_rejected_and_flagged():
+    """a^k = 0 leaves the slope identity undefined: create
+    rejects it (EINVAL); a zero slope set later gives a NaN slope gradient,
+    status bit 8 in loss column 5 and ENONFINITE from pinn_dd_step."""
+    from paper_2104_10013_b200.binding import PinnDDError, EINVAL, ENONFINITE, STATUS_SLOPE_ZERO
+    prob = make_config("C1", n_f=100, n_i=10, n_u=20)
+    lay = param_layout(prob.sizes)
+    oa = lay[1]["a"][0]
+    p0 = prob.subdomains[0].params.copy()
+    p0[oa] = 0.0
+    bad = dataclasses.replace(prob, subdomains=[dataclasses.replace(prob.subdomains[0], params=p0)]
+                              + prob.subdomains[1:])
     with pytest.raises(PinnDDError) as ei:
-        h.step(1)
-    assert ei.value.status == EPROTOCOL
-    h.close()
+        _handle(bad)
+    assert ei.value.status == EINVAL and "slope" in str(ei.value)
+    m = _handle(prob)
+    v = m.get(1, 0).clone()
+    v[oa] = 0.0
+    m.set(1, v, 0)
+    m.interface_payload()
+    loss, grad = m.loss_grad()
+    torch.cuda.synchronize()
+    assert int(loss[1, 5]) & STATUS_SLOPE_ZERO and int(loss[0, 5]) == 0
+    assert torch.isnan(grad[1, oa]) and torch.isfinite(grad[0]).all()
+    with pytest.raises(PinnDDError) as ei:
+        m.step(1)
+    assert ei.value.status == ENONFINITE and "slope" in str(ei.value)
+    m.close()
+
+
+def test_status_bits_reset_per_evaluation():
+    """A non-finite evaluation does not poison the next one: the status bits
+    are cleared at the start of every loss + gradient evaluation."""
+    from paper_2104_10013_b200.binding import PinnDDError, ENONFINITE
+    prob = make_config("C1", n_f=100, n_i=10, n_u=20)
+    m = _handle(prob)
+    good = m.get(0, 0).clone()
+    bad = good.clone()
+    bad[3] = float("nan")
+    m.set(0, bad, 0)
+    m.interface_payload()
+    loss, _ = m.loss_grad()
+    torch.cuda.synchronize()
+    assert int(loss[0, 5]) != 0
+    m.set(0, good, 0)
+    m.interface_payload()
+    loss, _ = m.loss_grad()
+    torch.cuda.synchronize()
+    assert torch.all(loss[:, 5] == 0)
+    m.step(1)          # no stale ENONFINITE
+    m.close()
 
 
 def test_data_parallel_pinn_shards_add_up():
@@ -584,8 +782,8 @@ def test_data_parallel_pinn_shards_add_up():
     assert (gs - gf).abs().max().item() <= 1e-5 * scale
     th = OL.init_state(prob).thetas
     ref = OL.loss_grad_all(prob, th)
-    check_loss(ls.cpu().numpy(), ref, "dp")
-    check_grad(gs, ref, prob.sizes, "dp", thetas=th)
+    check_loss(ls.cpu().numpy(), ref, loss_noise(prob, th), "dp")
+    check_grad(gs, ref, prob.sizes, th, "dp")
     # one data-parallel step (sum emulates the all-reduce)
     for r in reps:
         r.h.set(0, gs[0], what=3)
