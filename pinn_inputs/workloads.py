@@ -213,9 +213,34 @@ def _boundary_segments(lo, hi, dlo, dhi, pde):
     return segs
 
 
-def _targets(pde: str, x: np.ndarray, tag: str) -> Tuple[np.ndarray, np.ndarray]:
-    """Boundary / initial data of the paper's problems (inputs, not the method)."""
+def kovasznay(x: np.ndarray, re: float) -> np.ndarray:
+    """Kovasznay flow (exact steady NS solution, used as boundary data and as
+    the accuracy reference of f4): u = 1 - e^{lam x} cos 2 pi y,
+    v = lam/(2 pi) e^{lam x} sin 2 pi y, p = (1 - e^{2 lam x})/2,
+    lam = Re/2 - sqrt(Re^2/4 + 4 pi^2)."""
+    lam = re / 2.0 - np.sqrt(re * re / 4.0 + 4.0 * np.pi ** 2)
+    e = np.exp(lam * x[:, 0])
+    return np.stack([1.0 - e * np.cos(2 * np.pi * x[:, 1]), lam / (2 * np.pi) * e * np.sin(2 * np.pi * x[:, 1]),
+                     0.5 * (1.0 - e * e)], axis=1)
+
+
+def burgers_wave(x: np.ndarray, nu: float, a: float = 0.5, c: float = 0.2) -> np.ndarray:
+    """Viscous Burgers travelling wave u = c - a tanh(a (x - c t) / (2 nu))
+    (exact solution of u_t + u u_x = nu u_xx; boundary / initial data and
+    accuracy reference of f4)."""
+    return c - a * np.tanh(a * (x[:, 0] - c * x[:, 1]) / (2.0 * nu))
+
+
+def _targets(pde: str, x: np.ndarray, tag: str, bc: str = "paper", nu: float = 0.0,
+             re: float = 100.0) -> Tuple[np.ndarray, np.ndarray]:
+    """Boundary / initial data of the paper's problems (inputs, not the method).
+    bc = "kovasznay" (NS) / "wave" (Burgers): data of a closed-form solution
+    instead (accuracy tests of f4)."""
     n = len(x)
+    if pde == "burgers" and bc == "wave":
+        return burgers_wave(x, nu)[:, None], np.ones((n, 1))
+    if pde == "ns" and bc == "kovasznay":
+        return kovasznay(x, re), np.ones((n, 3))             # u, v and p (fixes the gauge)
     if pde == "burgers":
         # u(0,x) = -sin(pi x) on t = 0; u(t,+-1) = 0 (PAPER.md:316, 780)
         if tag == "x2lo":
@@ -255,7 +280,7 @@ def build_problem(*, name: str, pde: str, method: str, nx: int, ny: int,
                   nu: float = 0.01 / np.pi, re: float = 100.0,
                   weights=(20.0, 1.0, 20.0, 20.0),
                   betas=(0.9, 0.999), eps: float = 1e-8,
-                  n_f_per_sub: Optional[List[int]] = None) -> Problem:
+                  n_f_per_sub: Optional[List[int]] = None, bc: str = "paper") -> Problem:
     if method not in ("pinn", "cpinn", "xpinn", "hybrid"):
         raise ValueError(method)
     d_out = PDE_OUTPUTS[pde]
@@ -318,7 +343,7 @@ def build_problem(*, name: str, pde: str, method: str, nx: int, ny: int,
                 else:
                     x = np.stack([s, np.full(c, val)], axis=1)
                 x = _f32(x)
-                t, m = _targets(pde, x, tag)
+                t, m = _targets(pde, x, tag, bc, float(np.float32(nu)), float(np.float32(re)))
                 xs.append(x); ts.append(t); ms.append(m)
         if xs:
             x_u = np.concatenate(xs); u_t = np.concatenate(ts); u_m = np.concatenate(ms)
@@ -478,7 +503,7 @@ def make_config(cfg: str, *, scale: float = 1.0, method: Optional[str] = None,
     if n_hidden is not None:
         args["n_hidden"] = n_hidden
     for k in ("nx", "ny", "activation", "weights", "lr", "slope_n", "nu", "re", "pde", "seed_index",
-              "activations", "t_frac"):
+              "activations", "t_frac", "domain_lo", "domain_hi", "bc"):
         if k in kw:
             args[k] = kw[k]
     if cfg == "C5":

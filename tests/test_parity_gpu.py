@@ -118,7 +118,7 @@ def slope_bound(theta, g_ref, ent):
     return EPS32 * G / abs(theta[oa])
 
 
-def grad_noise(prob, thetas, samples=NOISE_SAMPLES):
+def grad_noise(prob, thetas, samples=6):
     """[n_sub][n_params] FP32 noise of the oracle gradient (module docstring);
     used where the loss is far from its seeded value (trained states), where
     the residuals F are small cancelling sums and so are the adjoint seeds."""
@@ -299,45 +299,47 @@ def test_adam_matches_oracle_on_gpu_gradient():
                                     ("C2", dict(method="xpinn", n_f=300, n_i=25, n_u=20)),
                                     ("C5", dict(scale=0.05, n_i=30, n_u=40))])
 def test_train_steps_track_oracle(cfg, kw):
-    """Parameters after 1 and 10 synchronous Algorithm-1 iterations
-    (graph-replayed) vs the oracle's iterations (Z18).  Adam's first steps move
-    a parameter by ~lr sign(g): an entry whose oracle gradient is ever within
-    1e-3 max|g| of its tensor of 0 can change sign or direction under the FP32
-    gradient error (up to ~1e-5 of the tensor max, measured), so it is
-    only held to the 2 lr t it can move; every other entry to
-    1e-5 |theta| + 1e-3 lr t.  Ambiguous entries must stay rare (< 5 %; 2-3 %
-    measured)."""
+    """10 consecutive synchronous Algorithm-1 iterations (Z18): at every
+    iteration t the GPU's parameters after the step are compared with one
+    oracle step (FP64 gradient + Adam) taken from the GPU's own (theta_t, m_t,
+    v_t, t) -- each step is held to the tolerance, without the chaotic
+    divergence of two free-running trajectories.  Every entry is held to
+    1e-5 |theta| + 1e-3 lr, except in the FIRST step, whose Adam update is
+    exactly lr sign(g): an entry whose oracle gradient is within 1e-3 of its
+    tensor's max|g| of 0 could flip sign under the FP32 gradient error (~1e-5
+    of the tensor max, measured), so those (< 5 %) are held to 2 lr there.
+    (Measured on the B200: every entry of every step agrees to <= 6e-8.)  The
+    reported J of each step matches the oracle's J at the parameters it was
+    evaluated at to 1.1e-5."""
     prob = make_config(cfg, **kw)
     m = _handle(prob)
-    st = OL.init_state(prob)
-    ambiguous = [np.zeros(n_params(prob.sizes), dtype=bool) for _ in range(prob.n_sub)]
     tens = _tensors(prob.sizes)
-    done = 0
-    for n_steps in (1, 10):
-        m.step(n_steps - done, want_loss=False)
-        while done < n_steps:
-            res = OL.loss_grad_all(prob, st.thetas)
-            th_new, ad_new = [], []
-            for q, (_, g) in enumerate(res):
-                gn = np.abs(g.numpy())
-                for _, o, n in tens:                    # per tensor, like the gradient tolerance
-                    ambiguous[q][o:o + n] |= gn[o:o + n] < 1e-3 * gn[o:o + n].max()
-                th, ad = OL.adam_step(st.thetas[q], g, st.adam[q], prob.lr, prob.beta1, prob.beta2, prob.eps)
-                th_new.append(th)
-                ad_new.append(ad)
-            st = OL.TrainState(th_new, ad_new)
-            done += 1
+    for t in range(10):
+        th = [m.get(q, 0).double().cpu() for q in range(prob.n_sub)]
+        mm = [m.get(q, 1).double().cpu() for q in range(prob.n_sub)]
+        vv = [m.get(q, 2).double().cpu() for q in range(prob.n_sub)]
+        assert all(m.adam_t(q) == t for q in range(prob.n_sub))
+        cur = dataclasses.replace(prob, subdomains=[dataclasses.replace(sd, params=p.numpy())
+                                                    for sd, p in zip(prob.subdomains, th)])
+        res = OL.loss_grad_all(cur, th)
+        out = m.step(1)
         torch.cuda.synchronize()
-        for q in range(prob.n_sub):
+        for q, (bd, g) in enumerate(res):
+            assert abs(out[q, 4] - bd.total) <= 1e-5 * abs(bd.total) + 1e-6 * abs(bd.total), (cfg, t, q)
+            want, _ = OL.adam_step(th[q], g, OL.AdamState(mm[q], vv[q], t), prob.lr, prob.beta1, prob.beta2,
+                                   prob.eps)
+            want = want.numpy()
             got = m.get(q, 0).double().cpu().numpy()
-            want = st.thetas[q].numpy()
+            gn = np.abs(g.numpy())
+            amb = np.zeros(gn.shape, dtype=bool)
+            if t == 0:
+                for _, o, n in tens:
+                    amb[o:o + n] = gn[o:o + n] < 1e-3 * gn[o:o + n].max()
             d = np.abs(got - want)
-            amb = ambiguous[q]
-            tol = 1e-5 * np.abs(want) + 1e-3 * prob.lr * n_steps
-            assert np.all(d[~amb] <= tol[~amb]), (cfg, n_steps, q, np.max(d[~amb] - tol[~amb]))
-            assert np.all(d[amb] <= 2 * prob.lr * n_steps + 1e-5 * np.abs(want[amb])), (cfg, n_steps, q)
-            assert amb.mean() < 0.05, (cfg, q, amb.mean())
-        assert all(m.adam_t(q) == n_steps for q in range(prob.n_sub))
+            tol = 1e-5 * np.abs(want) + 1e-3 * prob.lr
+            assert np.all(d[~amb] <= tol[~amb]), (cfg, t, q, np.max(d[~amb] - tol[~amb]))
+            assert np.all(d[amb] <= 2 * prob.lr + 1e-5 * np.abs(want[amb])), (cfg, t, q)
+            assert amb.mean() < 0.05, (cfg, t, q, amb.mean())
     m.close()
 
 

@@ -1,21 +1,19 @@
 #!/bin/bash
-# Copy gpurun_out/ev (tools/final_evidence.sh) into profiles/ and print the table.
+# Copy gpurun_out/ev (tools/final_evidence.sh) into profiles/ with a round tag
+# and print the table.  usage: collect_evidence.sh r02
 set -e
 cd "$(dirname "$0")/.."
-for f in gpurun_out/ev/bench_*.json; do b=$(basename $f .json); tail -1 $f > profiles/r01_final_$b.json; done
-cp gpurun_out/ev/launches_c2.csv profiles/r01_final_launches_c2_cpinn.csv
-cp gpurun_out/ev/pytest_gpu.txt profiles/r01_final_pytest_gpu.txt
-cp gpurun_out/ev/smoke.txt profiles/r01_final_smoke.txt
-rm -f profiles/k1_dram_bytes.json
-python tools/dram_table.py "C2-poisson-4x4-6x40 cpinn" gpurun_out/ev/k1_c2.ncu-rep "C3-burgers-xpinn-4x2-5x20 xpinn" \
-    gpurun_out/ev/k1_c3.ncu-rep "C4-ns-xpinn-4x2-5x80 xpinn" gpurun_out/ev/k1_c4.ncu-rep \
-    "C5-heatinv-xpinn-voronoi10-3x80 xpinn" gpurun_out/ev/k1_c5.ncu-rep > /dev/null
-for w in c2 c3 c4 c5; do
-  python tools/ncu_summary.py gpurun_out/ev/k1_$w.ncu-rep profiles/r01_final_k1_${w}_ncu_summary.json > /dev/null
-done
-for f in profiles/r01_final_bench_*.json; do python - "$f" <<'PY'
+R=${1:-r02}
+for f in gpurun_out/ev/bench_*.json; do b=$(basename $f .json); tail -1 $f > profiles/${R}_$b.json; done
+[ -f gpurun_out/ev/launches_c4.csv ] && cp gpurun_out/ev/launches_c4.csv profiles/${R}_launches_c4.csv
+[ -f gpurun_out/ev/pytest_gpu.txt ] && cp gpurun_out/ev/pytest_gpu.txt profiles/${R}_pytest_gpu.txt
+[ -f gpurun_out/ev/smoke.txt ] && cp gpurun_out/ev/smoke.txt profiles/${R}_smoke.txt
+for f in profiles/${R}_bench_*.json; do python - "$f" <<'PY'
 import json, sys
-d = json.loads(open(sys.argv[1]).read())
+try:
+    d = json.loads(open(sys.argv[1]).read())
+except Exception as e:
+    print(sys.argv[1], "unparsable", e); sys.exit(0)
 r = d.get("roofline") or {}
 c = d.get("cpu_baseline") or {}
 print(sys.argv[1].split("/")[-1], d["config"]["workload"], "%.4g" % d["value"], round(d["ms_per_step"], 4),

@@ -167,13 +167,16 @@ int run(const char* name, int v) {
   return bad;
 }
 
-int main() {
-  for (int v = 0; v < 4; ++v) run<128, 64, 32, 0>("A K-major SW32B  K=32 ", v);
-  for (int v = 0; v < 4; ++v) run<128, 64, 64, 0>("A K-major SW32B  K=64 ", v);
-  for (int v = 0; v < 4; ++v) run<128, 80, 80, 0>("A K-major SW32B  K=80 N=80", v);
-  for (int v = 0; v < 4; ++v) run<128, 64, 64, 1>("B K-major SW32B  K=64 ", v);
-  for (int v = 0; v < 4; ++v) run<128, 80, 80, 1>("B K-major SW32B  K=80 N=80", v);
-  for (int v = 0; v < 4; ++v) run<128, 64, 64, 2>("A MN-major SW32B + B K-major SW32B K=64", v);
-  for (int v = 0; v < 4; ++v) run<128, 80, 128, 2>("A MN-major SW32B + B K-major SW32B K=128 N=80", v);
-  return 0;
+int main(int argc, char** argv) {
+  // one (case, variant) per process: a bad descriptor faults the context
+  const int c = argc > 1 ? atoi(argv[1]) : 0, v = argc > 2 ? atoi(argv[2]) : 0;
+  switch (c) {
+    case 0: return run<128, 64, 32, 0>("A K-major SW32B  K=32 ", v);
+    case 1: return run<128, 64, 64, 0>("A K-major SW32B  K=64 ", v);
+    case 2: return run<128, 80, 80, 0>("A K-major SW32B  K=80 N=80", v);
+    case 3: return run<128, 64, 64, 1>("B K-major SW32B  K=64 ", v);
+    case 4: return run<128, 80, 80, 1>("B K-major SW32B  K=80 N=80", v);
+    case 5: return run<128, 64, 64, 2>("A MN-major SW32B + B K-major SW32B K=64", v);
+    default: return run<128, 80, 128, 2>("A MN-major SW32B + B K-major SW32B K=128 N=80", v);
+  }
 }
