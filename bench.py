@@ -337,7 +337,7 @@ def run_ours(args):
     import torch.distributed as dist
     import __graft_entry__ as ge
     ge.build()
-    from paper_2104_10013_b200.binding import PinnDD, FLAG_GRAPH, FLAG_TIMING
+    from paper_2104_10013_b200.binding import PinnDD, FLAG_GRAPH, FLAG_TIMING, FLAG_TF32
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -370,11 +370,12 @@ def run_ours(args):
         # N > 1: the library's NCCL transport, the whole iteration (exchange
         # included) one CUDA graph; N = 1: the fused single-GPU graph
         xp = dict(transport="nccl", world=world, group=group) if world > 1 else {}
-        h = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH, **xp)
+        fl = FLAG_GRAPH | (FLAG_TF32 if args.tf32 else 0)
+        h = PinnDD(prob, local, owner, rank, device=dev, flags=fl, **xp)
         # a second handle with event-record nodes in its graph: per-kernel times
         # (K1 roofline, compute / exchange split) in their own timed region, so
         # the headline timing carries no event nodes
-        ht = PinnDD(prob, local, owner, rank, device=dev, flags=FLAG_GRAPH | FLAG_TIMING, **xp)
+        ht = PinnDD(prob, local, owner, rank, device=dev, flags=fl | FLAG_TIMING, **xp)
         h_prob = prob
     stream = h.stream
     pts_local = h.n_points
@@ -528,7 +529,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "scaling": scaling, "vs_baseline": None, "dtype": "tf32" if args.tf32 else "f32",
             "data": "synthetic",
             "iters_per_s": 1e3 * args.steps / t_max,
             "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
@@ -593,6 +594,8 @@ def main():
                     help="default cpinn for c2, xpinn for c5; dp = data-parallel vanilla PINN comparator "
                          "(Table 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--tf32", action="store_true",
+                    help="hidden layers on the tensor cores (PINN_DD_FLAG_TF32, width-80 workloads c4 / c5)")
     ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c4",
                     help="c4: BASELINE configs[3] (default: the largest single-GPU config, strong); "
                          "c2: configs[1] (strong, 16/N subdomains per GPU); c3: configs[2] (weak, one "

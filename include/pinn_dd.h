@@ -87,6 +87,11 @@ enum { PINN_DD_PREDICT_STITCHED = 0,  /* Eq. (4): average of the owners' nets, w
 #define PINN_DD_FLAG_GRAPH        1  /* pinn_dd_step replays a captured CUDA graph */
 #define PINN_DD_FLAG_GLOBAL_STASH 2  /* keep the reverse-mode stash in global memory instead of TMEM (debug) */
 #define PINN_DD_FLAG_TIMING       4  /* record per-kernel CUDA events (see pinn_dd_kernel_times) */
+#define PINN_DD_FLAG_TF32         8  /* width-80 nets: hidden-layer contractions on the tensor cores
+                                        (tcgen05.mma kind::tf32, single-pass TF32 products, FP32
+                                        accumulation; looser tolerance, DESIGN.md 6 / 11).  Compiled
+                                        for [2, 80x5, 3] and [2, 80x3, 2] (per-subdomain activation);
+                                        other shapes: PINN_DD_EUNSUPPORTED */
 
 /* Status bits of one loss + gradient evaluation (loss column 5, per subdomain).
    A slope a^k that reaches 0 (set_params, or Adam) makes its gradient NaN. */

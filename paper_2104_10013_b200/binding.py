@@ -25,7 +25,7 @@ OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, ENONFINITE, EPROTOCOL = range(7)
 METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2, "hybrid": 3}
 PDES = {"burgers": 0, "poisson": 1, "heat": 2, "ns": 3, "heat_inv": 4}
 ACTS = {"tanh": 0, "sin": 1, "cos": 2}
-FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING = 1, 2, 4
+FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING, FLAG_TF32 = 1, 2, 4, 8
 GEOM_NONE, GEOM_BOXES, GEOM_VORONOI = 0, 1, 2
 PREDICT_STITCHED, PREDICT_OWNER = 0, 1
 STATUS_J, STATUS_GRAD, STATUS_SLOPE, STATUS_SLOPE_ZERO = 1, 2, 4, 8

@@ -20,6 +20,7 @@
 
 #include "../../include/pinn_dd.h"
 #include "pinn_dd_kernels.cuh"
+#include "pinn_dd_kernels_tc.cuh"
 
 using namespace pinn;
 
@@ -87,6 +88,7 @@ const Nccl& nccl() {
 // -------------------------------------------------------------------------
 struct Ops {
   int N, NH, DO, ACT;
+  int tc;          // 1: hidden layers on the tensor cores (tcgen05 kind::tf32, PINN_DD_FLAG_TF32)
   int pstride;     // Lay::total()
   int P;           // points per tile
   int threads;     // threads per CTA of the fused kernels
@@ -159,14 +161,51 @@ struct Inst {
   }
   static Ops ops() {
     static_assert(NH <= kMaxHidden, "too many hidden layers");
-    return Ops{N, NH, DO, ACT, LY::total(), C::P, T, C::CPS, smem(), &k1, &k2, &kf, &pred, &packmap, &slopetab,
+    return Ops{N, NH, DO, ACT, 0, LY::total(), C::P, T, C::CPS, smem(), &k1, &k2, &kf, &pred, &packmap, &slopetab,
                &setattr};
+  }
+};
+
+// tensor-core (TF32) instances of the width-80 shapes: same parameter layout,
+// planning and K5 / K6 as the FP32 instance, K1 / K2 / fused step = k_fused_tc
+template <int NH, int DO, int ACT>
+struct InstTc {
+  using F = Inst<80, NH, DO, ACT>;
+  using C = tc::TcCfg<NH, DO>;
+  static void k1(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_fused_tc<NH, DO, ACT, 0><<<grid, tc::T, sm, s>>>(a);
+  }
+  static void k2(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_fused_tc<NH, DO, ACT, 1><<<grid, tc::T, sm, s>>>(a);
+  }
+  static void kf(const KArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_fused_tc<NH, DO, ACT, 2><<<grid, tc::T, sm, s>>>(a);
+  }
+  static cudaError_t setattr(size_t sm) {
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaFuncSetAttribute(k_fused_tc<NH, DO, ACT, 0>, attr, int(sm));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused_tc<NH, DO, ACT, 1>, attr, int(sm));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_fused_tc<NH, DO, ACT, 2>, attr, int(sm));
+    return e;
+  }
+  static Ops ops() {
+    Ops o = F::ops();
+    o.tc = 1;
+    o.P = tc::P;
+    o.threads = tc::T;
+    o.cps = 1;
+    o.smem = C::SMEM;
+    o.k1 = &k1;
+    o.k2 = &k2;
+    o.kf = &kf;
+    o.setattr = &setattr;
+    return o;
   }
 };
 
 // The shapes of BASELINE.json configs C1-C4 (tanh): 3x20, 5x20, 6x40, 5x80 (D_o = 3);
 // C5 (inverse heat, outputs (T, K)): 3x80 with tanh / sin / cos per region (Table 3).
-const Ops* find_ops(int N, int NH, int DO, int ACT) {
+const Ops* find_ops(int N, int NH, int DO, int ACT, int tc) {
   static const Ops table[] = {
       // width 20: two 128-thread CTAs per SM (C3 K1 0.369 -> 0.285 ms)
       Inst<20, 3, 1, 0, 128>::ops(),  Inst<20, 5, 1, 0, 128>::ops(),
@@ -176,13 +215,15 @@ const Ops* find_ops(int N, int NH, int DO, int ACT) {
       Inst<40, 6, 1, 0, 128>::ops(),  Inst<40, 6, 1, 0>::ops(),
       // width 80: one 256-thread CTA per SM (the weights alone are 104 KB of shared memory)
       Inst<80, 5, 3, 0>::ops(),              Inst<80, 3, 2, kActMixed>::ops(),
+      // tensor-core hidden layers (PINN_DD_FLAG_TF32)
+      InstTc<5, 3, 0>::ops(),                InstTc<3, 2, kActMixed>::ops(),
   };
   // development knob: PINN_DD_CTA_THREADS=128|256 picks the CTA size where both exist
   const char* ev = std::getenv("PINN_DD_CTA_THREADS");
   const int thr = ev ? std::atoi(ev) : 0;
   const Ops* first = nullptr;
   for (const Ops& o : table)
-    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT) {
+    if (o.N == N && o.NH == NH && o.DO == DO && o.ACT == ACT && o.tc == tc) {
       if (!first) first = &o;
       if (thr == 0 || o.threads == thr) return &o;
     }
@@ -350,11 +391,15 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   }
   const int act0 = d->sub_activation ? d->sub_activation[0] : d->activation;
   // one compiled activation if uniform, else the per-subdomain (kActMixed) instance
-  const Ops* ops = mixed ? nullptr : find_ops(d->width, d->n_hidden, d->d_out, act0);
-  if (!ops) ops = find_ops(d->width, d->n_hidden, d->d_out, kActMixed);
+  const int tc = (d->flags & PINN_DD_FLAG_TF32) ? 1 : 0;
+  if (tc && (d->flags & PINN_DD_FLAG_GLOBAL_STASH))
+    return fail(h, PINN_DD_EUNSUPPORTED, "PINN_DD_FLAG_TF32 keeps its stash in TMEM (no global stash)");
+  const Ops* ops = mixed ? nullptr : find_ops(d->width, d->n_hidden, d->d_out, act0, tc);
+  if (!ops) ops = find_ops(d->width, d->n_hidden, d->d_out, kActMixed, tc);
   if (!ops)
-    return fail(h, PINN_DD_EUNSUPPORTED, "network [2, %dx%d, %d] activation %d%s not compiled in", d->width,
-                d->n_hidden, d->d_out, act0, mixed ? " (mixed per subdomain)" : "");
+    return fail(h, PINN_DD_EUNSUPPORTED, "network [2, %dx%d, %d] activation %d%s%s not compiled in", d->width,
+                d->n_hidden, d->d_out, act0, mixed ? " (mixed per subdomain)" : "",
+                tc ? " with tensor-core (TF32) layers" : "");
   if (d->n_sub < 1) return fail(h, PINN_DD_EINVAL, "n_sub must be >= 1");
   if (!d->sub_point_offset || !d->sub_n_res || !d->sub_n_data || !d->sub_seg_offset || !d->sub_hparams)
     return fail(h, PINN_DD_EINVAL, "subdomain arrays must not be NULL");

@@ -794,3 +794,83 @@ def test_data_parallel_pinn_shards_add_up():
     assert torch.equal(p0, p1)
     for r in reps + [full]:
         (r.close() if hasattr(r, "close") else None)
+
+
+# --------------------------------------------------------------------------
+# Tensor-core hidden layers (PINN_DD_FLAG_TF32, DESIGN.md 6/11):
+# single-pass TF32 products (unit roundoff eps_tf32 = 2^-11), FP32 elsewhere.
+# Stated tolerances (measured worst in profiles/r02_tf32_err.txt): loss terms
+# 5e-3 relative (2.4e-3) + the noise model scaled by eps_tf32 / eps32 = 2^13;
+# W / b gradients 5e-3 of the tensor max (1.9e-3); slopes
+# 1e-2 |g_a| + eps_tf32 G_a / |a^k| (the slope identity's conditioning, §5.3).
+# --------------------------------------------------------------------------
+
+EPS_TF32 = 2.0 ** -11
+TF32_CASES = [("C4", dict(method="xpinn", n_f=150, n_i=20, n_u=16)),
+              ("C4", dict(method="cpinn", n_f=150, n_i=20, n_u=16)),
+              ("C4", dict(method="xpinn", n_f=6400, n_i=64, n_u=40)),     # 4-tile chunks
+              ("C5", dict(scale=0.1, n_i=24, n_u=40)),
+              ("C5", dict(scale=0.05, n_i=24, n_u=40, activations=["cos"] * 10))]
+
+
+@pytest.mark.parametrize("cfg,kw", TF32_CASES)
+@pytest.mark.parametrize("pert", [0.0, 0.2])
+def test_tf32_tensor_core_parity(cfg, kw, pert):
+    from paper_2104_10013_b200.binding import FLAG_GRAPH, FLAG_TF32
+    prob = make_config(cfg, **kw)
+    if pert:
+        prob = perturb_params(prob, scale=pert)
+    m = _handle(prob, flags=FLAG_GRAPH | FLAG_TF32)
+    m.interface_payload()
+    loss, grad = m.loss_grad()
+    torch.cuda.synchronize()
+    th = OL.init_state(prob).thetas
+    ref = OL.loss_grad_all(prob, th)
+    noise = loss_noise(prob, th) * 2.0 ** 13
+    l = loss.cpu().numpy()
+    for q, (bd, g) in enumerate(ref):
+        want = bd.as_list()
+        for i in range(5):
+            tol = 5e-3 * abs(want[i]) + NOISE_K * noise[q, i]
+            assert abs(float(l[q, i]) - want[i]) <= tol, (cfg, q, i, float(l[q, i]), want[i])
+        assert l[q, 5] == 0
+        gg = grad[q].double().cpu().numpy()
+        gr = g.numpy()
+        tq = th[q].numpy()
+        for ent in param_layout(prob.sizes):
+            for key in ("W", "b"):
+                o, n = ent[key]
+                den = np.abs(gr[o:o + n]).max()
+                assert np.abs(gg[o:o + n] - gr[o:o + n]).max() <= 5e-3 * den, (cfg, q, key)
+            if "a" in ent:
+                oa = ent["a"][0]
+                bound = 1e-2 * abs(gr[oa]) + slope_bound(tq, gr, ent) * EPS_TF32 / EPS32
+                assert abs(gg[oa] - gr[oa]) <= bound, (cfg, q, "a", gg[oa], gr[oa], bound)
+    m.close()
+
+
+def test_tf32_fused_step_equals_phased_and_trains():
+    """The tensor-core kernel's fused step (payload chunks + loss chunks in one
+    launch) equals its phased calls bitwise, and 300 graph-replayed TF32
+    steps reduce J on C4 like the FP32 kernel does (relative difference of the
+    final J < 5 %)."""
+    from paper_2104_10013_b200.binding import FLAG_GRAPH, FLAG_TF32
+    prob = make_config("C4", method="xpinn", n_f=800, n_i=40, n_u=40)
+    a = _handle(prob, flags=FLAG_GRAPH | FLAG_TF32)
+    assert a.step_fused
+    out = a.step(1)
+    b = _handle(prob, flags=FLAG_GRAPH | FLAG_TF32)
+    b.interface_payload()
+    lb, gb = b.loss_grad()
+    b.adam()
+    torch.cuda.synchronize()
+    for q in range(prob.n_sub):
+        assert np.array_equal(np.asarray(out[q, :5]), lb[q, :5].cpu().numpy()), q
+        assert torch.equal(a.get(q, 3), b.get(q, 3)) and torch.equal(a.get(q, 0), b.get(q, 0)), q
+    f = _handle(prob)
+    f.step(1)
+    j32 = f.step(300)[:, 4].sum()
+    jt = a.step(300)[:, 4].sum()
+    assert jt < 0.5 * out[:, 4].sum() and abs(jt - j32) < 0.05 * j32, (jt, j32)
+    for h in (a, b, f):
+        h.close()
