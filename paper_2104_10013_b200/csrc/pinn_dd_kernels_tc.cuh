@@ -26,10 +26,11 @@
 //
 // TMEM (512 columns): R = [0, 80) input adjoint; S_k = [80 k, 80 k + 80) the
 // pre-activation jets of layer k (the forward MMA's accumulator, rewritten in
-// stash form: t = tanh(s z) for tanh), k = 1..NH; dW^k's 96-column
-// accumulator reuses S_k (+16 columns of the consumed S_{k+1}) after the
-// reverse sweep has read it.  The chunk's gradient partial is read-modify-
-// written once per tile and layer, coalesced through a shared staging copy.
+// stash form: t = tanh(s z) for tanh), k = 1..NH; the accumulator of
+// dW^k^T (96 lanes x 80 columns) reuses S_k after the
+// reverse sweep has read it.  dW^k is computed transposed (lanes = inputs i,
+// columns = neurons j), so adding it into the chunk's gradient partial is a
+// coalesced stream of fire-and-forget reductions (one per entry per tile).
 //
 // Precision: single-pass TF32 products (10-bit mantissa, FP32 accumulate);
 // activations, loss, adjoint seeds and every reduction stay FP32.  The looser
@@ -50,7 +51,6 @@ constexpr int T = 256;       // threads per CTA
 constexpr int CP = 96;       // padded contiguous extent of an operand row (3 atoms of 32)
 constexpr int NA = CP / 32;  // atoms per 4-row group
 constexpr int KF = 88;       // forward K: 80 inputs + the ones (bias) column, rounded to 8
-constexpr int ND = 96;       // dW accumulator columns: 80 + db column + padding
 constexpr int OPER = M * CP; // floats of an activation operand buffer
 constexpr int WOPER = N * CP;   // floats of one W operand
 constexpr int TCOLS = 512;   // TMEM columns allocated
@@ -138,6 +138,19 @@ __device__ __forceinline__ void ld32x16(uint32_t a, uint32_t* r) {
       : "memory");
 }
 
+__device__ __forceinline__ void ld32x8(uint32_t a, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(a)
+               : "memory");
+}
+// fire-and-forget add into the chunk partial.  Each partial entry is added to
+// by one thread only (fixed thread <-> entry map, tiles of a chunk in order),
+// so the adds land in program order: the sum is deterministic.
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 // the thread's view of a tile: point pt (0..31), quarter q, half hf, lane-in-quarter rows
 struct Who {
   int q, hf, a, pp, pt;
@@ -201,13 +214,13 @@ struct TcCfg {
   // shared-memory carve (floats); operands first (1024-B aligned)
   static constexpr int oW = 0;                               // (NH-1) x [80 rows j][96] W^k | b^k
   static constexpr int oH = oW + (NH - 1) * WOPER;           // [128 m][96] H^{k-1} (+ ones column 80)
-  static constexpr int oZ = oH + OPER;                       // [128 m][96] Zb^k; also the dW staging copy
+  static constexpr int oZ = oH + OPER;                       // [128 m][96] Zb^k
   // while Zb^k is not live (output layer, layer 1) its buffer also holds the
   // output-layer partials [2 halves][P][DO] float4 and the per-quarter
-  // reduction scratch [4][N][4]; the dW staging copy [80][81] stays below
-  static constexpr int oUp = oZ + 8192;
+  // reduction scratch [4][N][4]
+  static constexpr int oUp = oZ;
   static constexpr int oRed = oUp + 2 * 4 * P * DO;
-  static_assert(N * (N + 1) <= 8192 && oRed + 4 * N * 4 <= oZ + OPER, "aliases inside the Zb buffer");
+  static_assert(oRed + 4 * N * 4 <= oZ + OPER, "aliases inside the Zb buffer");
   static constexpr int oW1 = oZ + OPER;                      // (the MN-major dW read of Zb runs 512 B past it)
   static constexpr int oB1 = oW1 + 2 * N;
   static constexpr int oWo = oB1 + N;                        // [DO][80]
@@ -216,11 +229,11 @@ struct TcCfg {
   static constexpr int oX = al4(oSl + NH);                   // [2][P]
   static constexpr int oU = oX + 2 * P;                      // [P][DO] float4
   static constexpr int oMisc = oU + 4 * P * DO;              // loss scratch [8][4], mbarrier, tmem slot, s_next
-  static constexpr int TOTAL = oMisc + 32 + 8;
+  static constexpr int TOTAL = oMisc + 32 + 8;   // loss scratch, 2 mbarriers, tmem slot, s_next
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget of the tensor-core kernel");
   static_assert((oH * 4) % 1024 == 0 && (oZ * 4) % 1024 == 0 && (WOPER * 4) % 1024 == 0, "operand alignment");
-  static_assert(80 * NH + ND <= TCOLS + 80 - 80 && 80 * (NH + 1) <= TCOLS, "TMEM columns");
+  static_assert(80 * (NH + 1) <= TCOLS, "TMEM columns");
 };
 
 }  // namespace tc
@@ -251,9 +264,10 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   float4* sUp = reinterpret_cast<float4*>(sm + C::oUp);
   float* sRed = sm + C::oRed;
   float* sLoss = sm + C::oMisc;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + C::oMisc + 32);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::oMisc + 34);
-  int* s_next = reinterpret_cast<int*>(sm + C::oMisc + 35);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + C::oMisc + 32);    // forward / input-adjoint MMAs
+  uint64_t* mbar2 = reinterpret_cast<uint64_t*>(sm + C::oMisc + 34);   // dW MMAs
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::oMisc + 36);
+  int* s_next = reinterpret_cast<int*>(sm + C::oMisc + 37);
   const float m1 = a.m1, m2 = a.m2;
   const uint32_t aH = smem_u32(sH), aZ = smem_u32(sZ), aW = smem_u32(sW);
 
@@ -264,7 +278,10 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     sH[sw32(r, c)] = (c == N && ((r >> 3) & 3) == 0) ? 1.0f : 0.0f;
   }
   for (int e = tid; e < M * (CP - N); e += T) sZ[sw32(e / (CP - N), N + e % (CP - N))] = 0.0f;
-  if (tid == 0) mbar_init(mbar);
+  if (tid == 0) {
+    mbar_init(mbar);
+    mbar_init(mbar2);
+  }
   if (tid < 32) {
     __syncwarp();
     tmem_alloc<TCOLS>(tslot);
@@ -274,7 +291,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   cta_sync();
   tmem_fence_after();
   const uint32_t tm = *tslot;
-  uint32_t phase = 0;
+  uint32_t phase = 0, phase2 = 0;
   // one elected thread issues a group of MMAs after every thread's operand
   // writes (generic proxy) are fenced into the async proxy
   auto issue = [&](auto body) {
@@ -456,15 +473,56 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             const float v = ((sRed[(0 * N + j) * 4 + o] + sRed[(1 * N + j) * 4 + o]) + sRed[(2 * N + j) * 4 + o]) +
                             sRed[(3 * N + j) * 4 + o];
             float* g = Pc + LY::offW(NH + 1) + e;
-            *g = first ? v : __ldcg(g) + v;
+            if (first)
+              *g = v;
+            else
+              red_add(g, v);
           }
           if (tid < DO) {
             float v = 0.0f;
             for (int p = 0; p < P; ++p) v += sU[p * DO + tid].x;
             float* g = Pc + LY::offB(NH + 1) + tid;
-            *g = first ? v : __ldcg(g) + v;
+            if (first)
+              *g = v;
+            else
+              red_add(g, v);
           }
-          // hidden layers k = NH .. 2
+          cta_sync();   // sRed / sUp (inside the Zb buffer) are read before Zb is written
+          // hidden layers k = NH .. 2.  Per step: the input-adjoint MMA commits to
+          // mbar, the dW MMA to mbar2, so the dW MMA runs while the threads read
+          // Hb^{k-1} and compute the next step's activation maps; its result
+          // (dW^k^T in S_k: lanes i, columns j) is added to the chunk partial
+          // just before the next operands overwrite its inputs.
+          int pend = 0;   // layer whose dW^T waits in TMEM (0 = none)
+          auto flush_dw = [&]() {
+            if (!pend) return;
+            mbar_wait(mbar2, phase2);
+            phase2 ^= 1u;
+            tmem_fence_after();
+            if (w.q < 3) {   // lanes i = 0..95 (i < 80: W^k column i; i = 80: b^k)
+              uint32_t r[5][8];
+#pragma unroll
+              for (int b = 0; b < 5; ++b)
+                ld32x8(tm + (uint32_t(32 * w.q) << 16) + uint32_t(80 * pend + 40 * w.hf + 8 * b), r[b]);
+              ld_wait();
+              const int i = 32 * w.q + (tid & 31);
+              if (i <= N) {
+                float* g = i < N ? Pc + LY::offW(pend) + 40 * w.hf * N + i : Pc + LY::offB(pend) + 40 * w.hf;
+                const int st = i < N ? N : 1;
+#pragma unroll
+                for (int b = 0; b < 5; ++b)
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    float* gp = g + (8 * b + e) * st;
+                    if (first)
+                      *gp = __uint_as_float(r[b][e]);
+                    else
+                      red_add(gp, __uint_as_float(r[b][e]));
+                  }
+              }
+            }
+            pend = 0;
+          };
 #pragma unroll 1
           for (int k = NH; k >= 2; --k) {
             tload(tm, w, 80 * k, z);
@@ -479,64 +537,35 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
 #pragma unroll
               for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
             }
-            tmem_fence_before();
-            cta_sync();   // the previous MMAs' operands and the staging copy are consumed
+            flush_dw();   // the previous dW MMA has read Zb / H: they may be overwritten
             owrite(sZ, w, hb);   // Zb^k
             owrite(sH, w, z);    // H^{k-1}
             const uint32_t wk = aW + uint32_t((k - 2) * WOPER * 4);
-            issue([&] {
+            fence_async_smem();
+            tmem_fence_before();
+            cta_sync();
+            if (tid == 0) {
+              tmem_fence_after();
               // Hb^{k-1} = Zb^k W^k : A = Zb (K-major, K = j), B = W^k (MN-major, N = i)
 #pragma unroll 1
               for (int ks = 0; ks < N / 8; ++ks) mma(tm, kmajor(aZ, ks), mnmajor(wk, ks), idesc(M, N, 0, 1), ks > 0);
-              // dW^k = Zb^T H : A = Zb (MN-major, M = j), B = H (MN-major, N = i + ones)
+              commit(mbar);
+              // dW^k^T = H^T Zb : A = H (MN-major, M = i + ones column), B = Zb (MN-major, N = j),
+              // into S_k (consumed above)
 #pragma unroll 1
               for (int ks = 0; ks < M / 8; ++ks)
-                mma(tm + uint32_t(80 * k), mnmajor(aZ, ks), mnmajor(aH, ks), idesc(M, ND, 1, 1), ks > 0);
-            });
-            // dW^k rows j (TMEM lanes) -> staging copy [j][81] in sZ -> coalesced
-            // read-modify-write of the chunk partial (W^k row-major, then b^k)
-            if (w.q < 3) {
-              const int j = 32 * w.q + (tid & 31);
-              uint32_t r[3][16];
-#pragma unroll
-              for (int b = 0; b < 3; ++b)
-                ld32x16(tm + (uint32_t(32 * w.q) << 16) + uint32_t(80 * k + 48 * w.hf + 16 * b), r[b]);
-              ld_wait();
-              if (j < N) {
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                  for (int e = 0; e < 16; ++e) {
-                    const int i = 48 * w.hf + 16 * b + e;
-                    if (i <= N) sZ[j * (N + 1) + i] = __uint_as_float(r[b][e]);
-                  }
-              }
+                mma(tm + uint32_t(80 * k), mnmajor(aH, ks), mnmajor(aZ, ks), idesc(M, N, 1, 1), ks > 0);
+              commit(mbar2);
             }
-            // Hb^{k-1} from R
-            tload(tm, w, 0, hb);
-            cta_sync();
-            {
-              float* gW = Pc + LY::offW(k);
-              float* gB = Pc + LY::offB(k);
-              constexpr int NE = N * N;
-              constexpr int IT = (NE + T - 1) / T;
-              float cur[IT];
-#pragma unroll
-              for (int it = 0; it < IT; ++it) {
-                const int e = tid + it * T;
-                cur[it] = (!first && e < NE) ? __ldcg(gW + e) : 0.0f;
-              }
-#pragma unroll
-              for (int it = 0; it < IT; ++it) {
-                const int e = tid + it * T;
-                if (e < NE) gW[e] = cur[it] + sZ[(e / N) * (N + 1) + e % N];
-              }
-              if (tid < N) gB[tid] = (first ? 0.0f : __ldcg(gB + tid)) + sZ[tid * (N + 1) + N];
-            }
+            pend = k;
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+            tmem_fence_after();
+            tload(tm, w, 0, hb);   // Hb^{k-1} from R
           }
+          flush_dw();
           // layer 1: Zb^1 = act_bwd(S_1, Hb^1); dW^1[j] = sum_p (zb_v x_p + zb_{d_i}), db^1 = sum_p zb_v
           tload(tm, w, 80, z);
-          cta_sync();   // the last staging copy (aliasing sRed's buffer) has been read
           {
             const float s = sSl[0];
             const float x = sX[w.pt], y = sY[w.pt];
@@ -564,7 +593,10 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             const float sum = ((sRed[(0 * N + j) * 4 + v] + sRed[(1 * N + j) * 4 + v]) + sRed[(2 * N + j) * 4 + v]) +
                               sRed[(3 * N + j) * 4 + v];
             float* g = Pc + (v < 2 ? LY::offW(1) + 2 * j + v : LY::offB(1) + j);
-            *g = first ? sum : __ldcg(g) + sum;
+            if (first)
+              *g = sum;
+            else
+              red_add(g, sum);
           }
           cta_sync();
         }
