@@ -102,6 +102,11 @@ def workload(name, method, world):
     if name == "c3":
         prob = make_config("C3", method=method, gpus=world)        # one subdomain per GPU
         return prob, list(range(prob.n_sub)), "weak"
+    if name == "c3x8":
+        # SURVEY 8(d) C3 variant: 8 subdomains (a 4 x 2 x-t block, 20k residual points
+        # each) per GPU, blocks side by side in x: (4N) x 2 subdomains on [-1, 1] x [0, 1]
+        prob = make_config("C3", method=method, gpus=8, nx=4 * world, ny=2)
+        return prob, [s.ix // 4 for s in prob.subdomains], "weak"
     if name == "c5":
         prob = make_config("C5", method=method)
         return prob, lpt_owner([prob.n_points(q) for q in range(prob.n_sub)], world), "strong"
@@ -596,10 +601,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--tf32", action="store_true",
                     help="hidden layers on the tensor cores (PINN_DD_FLAG_TF32, width-80 workloads c4 / c5)")
-    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c4",
+    ap.add_argument("--workload", choices=["c2", "c3", "c3x8", "c4", "c5"], default="c4",
                     help="c4: BASELINE configs[3] (default: the largest single-GPU config, strong); "
                          "c2: configs[1] (strong, 16/N subdomains per GPU); c3: configs[2] (weak, one "
-                         "subdomain per GPU); c5: configs[4] (LPT placement, strong)")
+                         "subdomain per GPU); c3x8: its variant with a 4x2 block of subdomains per GPU "
+                         "(weak); c5: configs[4] (LPT placement, strong)")
     args = ap.parse_args()
     if args.method is None:
         args.method = "cpinn" if args.workload == "c2" else "xpinn"

@@ -307,8 +307,10 @@ pinn_dd_status fail(pinn_dd* h, pinn_dd_status s, const char* fmt, ...) {
 
 int n_eq_of(int pde) { return pde == PINN_DD_PDE_NS ? 3 : 1; }
 
-// Tiles per full chunk of a run of `cnt` points: at most ~128 chunks per run
-// (1024 for giant runs, below).
+// Tiles per full chunk of a run of `cnt` points: at most ~148 chunks per run
+// (one per SM, so that ONE subdomain alone -- a GPU's share under strong
+// scaling at 8 GPUs -- still fills the persistent grid: C4 at 8 GPUs 126 ->
+// 148 chunks; 296 measured 4 % slower at 1 GPU; 1024 for giant runs, below).
 // Runs of >= 200 tiles use chunks of >= m tiles, m = ACC / 2048 clamped to
 // [1, 4] (ACC = floats of a chunk's gradient partial, flushed once per chunk
 // and read back by K5a: 6x40 -> 4, 5x20 -> 1, i.e. 3-tile chunks for C3's
@@ -326,7 +328,7 @@ int chunk_tiles(int cnt, int P, int acc) {
   // a giant run (the data-parallel comparator's single subdomain: 7,530 tiles
   // of 32) would get only ~128 chunks -- fewer than the persistent CTAs -- so
   // runs of > 2048 tiles with partials of <= 64 KB may use up to 1024 chunks
-  const int max_chunks = (tiles > 2048 && acc <= 16384) ? 1024 : 128;
+  const int max_chunks = (tiles > 2048 && acc <= 16384) ? 1024 : 148;
   return std::max(min_tiles, (tiles + max_chunks - 1) / max_chunks);
 }
 

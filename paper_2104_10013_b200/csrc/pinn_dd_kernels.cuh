@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   // payload chunks (K2's work), then the loss chunks; an interface loss chunk
   // waits until every payload chunk is done (all CTAs are resident and payload
   // chunks are handed out first, so the wait always ends).
-  __shared__ int s_next;
+  int& s_next = *reinterpret_cast<int*>(sm + C::TOTAL - 3);   // next chunk index (dynamic smem, after tslot)
   int cur_sub = -1;
   const int n_pay = MODE == 2 ? a.n_chunks2 : 0;
 #pragma unroll 1
@@ -831,6 +831,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   }
   if constexpr (MODE != 1) {
     if (a.gstash == nullptr) {
+      tmem_fence_before();
       cta_sync();
       tmem_fence_after();
       if (tid < 32) {

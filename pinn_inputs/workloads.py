@@ -506,6 +506,8 @@ def make_config(cfg: str, *, scale: float = 1.0, method: Optional[str] = None,
               "activations", "t_frac", "domain_lo", "domain_hi", "bc"):
         if k in kw:
             args[k] = kw[k]
+    if cfg == "C3" and ("nx" in kw or "ny" in kw):
+        args["name"] = f"C3-burgers-{args['method']}-{args['nx']}x{args['ny']}-5x20"
     if cfg == "C5":
         return build_voronoi_problem(**args)
     return build_problem(**args)

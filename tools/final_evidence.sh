@@ -29,6 +29,9 @@ bench)
   python bench.py --workload c2 --method hybrid --no-cpu > $O/bench_c2_hybrid.json 2>&1
   python bench.py --workload c2 --method dp --no-cpu > $O/bench_c2_dp.json 2>&1
   python bench.py --workload c3 > $O/bench_c3.json 2>&1
+  python bench.py --workload c3x8 --no-cpu > $O/bench_c3x8.json 2>&1
+  python bench.py --tf32 --no-cpu > $O/bench_c4_tf32.json 2>&1
+  python bench.py --workload c5 --tf32 --no-cpu > $O/bench_c5_tf32.json 2>&1
   python bench.py --workload c5 > $O/bench_c5.json 2>&1
   python bench.py --impl reference --steps 20 --warmup 3 > $O/bench_reference_c4.json 2>&1
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c4.csv \
