@@ -508,7 +508,8 @@ def run_ours(args):
     # capture (tools/dram_table.py); null when no capture of this workload exists
     traffic = None
     prof = os.path.join(ROOT, "profiles", "k1_dram_bytes.json")
-    wl_key = f"{h_prob.name} {'data-parallel PINN' if dp is not None else h_prob.method}"
+    wl_key = f"{h_prob.name} {'data-parallel PINN' if dp is not None else h_prob.method}" + \
+        (" tf32" if args.tf32 else "")
     if os.path.exists(prof) and world == 1:
         try:
             ent = json.load(open(prof)).get(wl_key)
@@ -527,10 +528,37 @@ def run_ours(args):
         if world == 1 and not args.no_cpu and dp is None:
             base = cpu_baseline(prob)
         acts = sorted({h_prob.act(q) for q in local})
-        kname = (f"K1 k_fused<{h_prob.width},{h_prob.n_hidden},{h_prob.d_out},"
+        kname = (f"K1 k_fused{'_tc' if args.tf32 else ''}<{h_prob.width},{h_prob.n_hidden},{h_prob.d_out},"
                  f"{'mixed' if len(acts) > 1 else acts[0]}> (fused fwd jets + loss + reverse"
                  f"{'; K2 interface payload in the same launch' if fused else ''})")
         share = k1_ms / (sum(tstep_ms) / n_t)
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
+                "frac": achieved / peak_fp32, "traffic": traffic,
+                "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md clocks.max.sm)"}
+        if args.tf32:
+            # tensor-core mode: the hidden-layer contractions (forward, input
+            # adjoint, dW: 3 x (NH-1) x 2 C N^2 FLOP per point with C jets) run as
+            # tcgen05 kind::tf32 MMAs; roofline against the dense TF32 peak = the
+            # measured dense BF16 peak x the nominal TF32 / BF16 ratio 1/2
+            try:
+                bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+                src = "MEASURED_PEAKS.json bf16_tflops x 1/2 (nominal TF32 / BF16 ratio)"
+            except Exception:
+                bf16, src = 2250.0, "nominal 2.25 PFLOP/s BF16 x 1/2 (MEASURED_PEAKS.json absent)"
+            N, NH = h_prob.width, h_prob.n_hidden
+            gemm = 0.0
+            for q in local:
+                s_ = h_prob.subdomains[q]
+                ni = sum(len(h_prob.edges[e].pts) for e in s_.edges)
+                cf = 2 if h_prob.method == "cpinn" else 4
+                gemm += (len(s_.x_f) * 4 + len(s_.x_u) * 1 + ni * cf) * 3 * (NH - 1) * 2 * N * N
+                gemm += ni * cf * (NH - 1) * 2 * N * N if fused else 0       # K2's forward in the fused launch
+            ach_t = gemm / (k1_ms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach_t, "peak": bf16 / 2, "unit": "TFLOP/s",
+                    "frac": ach_t / (bf16 / 2), "traffic": traffic, "peak_source": src,
+                    "tensor_gflop_per_launch": gemm / 1e9,
+                    "alu_view": {"achieved_all_flops": achieved, "fp32_peak": peak_fp32,
+                                 "frac": achieved / peak_fp32}}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
@@ -550,12 +578,10 @@ def run_ours(args):
                                        f"domain decomposition, {len(local)} subdomains/GPU"
                                        if dp is None else "data-parallel replicas, gradient all-reduce"),
                        "l2": "flushed (256 MiB write) between timed steps"},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_fp32, "unit": "TFLOP/s",
-                         "frac": achieved / peak_fp32, "traffic": traffic,
+            "roofline": {**roof,
                          "kernel": kname,
                          "k1_ms_per_launch": k1_ms, "k1_timing": k1_what, "k1_gflop_per_launch": k1_flops / 1e9,
                          "k1_share_of_step": share,
-                         "peak_source": "148 SM x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md clocks.max.sm)",
                          "hbm": {"algorithmic_bytes_per_launch": alg_bytes,
                                  "algorithmic_gbs": alg_bytes / (k1_ms * 1e-3) / 1e9,
                                  "traffic_gbs": (traffic / (k1_ms * 1e-3) / 1e9) if traffic else None,
