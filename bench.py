@@ -357,6 +357,7 @@ def run_ours(args):
         group = dist.group.WORLD
 
     dp = None
+    transport = None
     if args.method == "dp":
         # data-parallel vanilla PINN comparator: one 6x40 network on
         # [0,G]x[0,1] with C2's point count per GPU, points sharded, gradient all-reduce
@@ -374,13 +375,25 @@ def run_ours(args):
         local = [q for q in range(prob.n_sub) if owner[q] == rank]
         # N > 1: the library's NCCL transport, the whole iteration (exchange
         # included) one CUDA graph; N = 1: the fused single-GPU graph
-        xp = dict(transport="nccl", world=world, group=group) if world > 1 else {}
         fl = FLAG_GRAPH | (FLAG_TF32 if args.tf32 else 0)
-        h = PinnDD(prob, local, owner, rank, device=dev, flags=fl, **xp)
+        transport = args.transport if world > 1 else None
+
+        def make(flags, tr):
+            xp = dict(transport=tr, world=world, group=group) if tr else {}
+            return PinnDD(prob, local, owner, rank, device=dev, flags=flags, **xp)
+        try:
+            h = make(fl, transport)
+        except Exception as e:
+            if transport != "peer":
+                raise
+            # CUDA IPC between the ranks unavailable: every rank falls back to NCCL together
+            print(f"[bench] peer stores unavailable ({e}); NCCL transport", file=sys.stderr)
+            transport = "nccl"
+            h = make(fl, transport)
         # a second handle with event-record nodes in its graph: per-kernel times
         # (K1 roofline, compute / exchange split) in their own timed region, so
         # the headline timing carries no event nodes
-        ht = PinnDD(prob, local, owner, rank, device=dev, flags=fl | FLAG_TIMING, **xp)
+        ht = make(fl | FLAG_TIMING, transport)
         h_prob = prob
     stream = h.stream
     pts_local = h.n_points
@@ -573,8 +586,10 @@ def run_ours(args):
                        "subdomains_per_gpu": len(local), "points_per_step": int(pts_all.item()),
                        "net": f"2-{h_prob.width}x{h_prob.n_hidden}-{h_prob.d_out} {'/'.join(acts)}, "
                               "adaptive slope n=10",
-                       "parallelism": (f"domain decomposition, {len(local)} subdomains/GPU, neighbour-only NCCL "
-                                       "send/recv inside the library's step graph" if world > 1 and dp is None else
+                       "parallelism": (f"domain decomposition, {len(local)} subdomains/GPU, neighbour-only exchange "
+                                       + ("by peer stores inside the fused launch (CUDA IPC over NVLink)"
+                                          if transport == "peer" else "by NCCL send/recv inside the step graph")
+                                       if world > 1 and dp is None else
                                        f"domain decomposition, {len(local)} subdomains/GPU"
                                        if dp is None else "data-parallel replicas, gradient all-reduce"),
                        "l2": "flushed (256 MiB write) between timed steps"},
@@ -625,6 +640,9 @@ def main():
                     help="default cpinn for c2, xpinn for c5; dp = data-parallel vanilla PINN comparator "
                          "(Table 2)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: cut-edge rows by stores into the neighbours' memory inside the fused launch "
+                         "(default), or NCCL send/recv captured in the step graph")
     ap.add_argument("--tf32", action="store_true",
                     help="hidden layers on the tensor cores (PINN_DD_FLAG_TF32, width-80 workloads c4 / c5)")
     ap.add_argument("--workload", choices=["c2", "c3", "c3x8", "c4", "c5"], default="c4",

@@ -87,6 +87,8 @@ enum { PINN_DD_PREDICT_STITCHED = 0,  /* Eq. (4): average of the owners' nets, w
 #define PINN_DD_FLAG_GRAPH        1  /* pinn_dd_step replays a captured CUDA graph */
 #define PINN_DD_FLAG_GLOBAL_STASH 2  /* keep the reverse-mode stash in global memory instead of TMEM (debug) */
 #define PINN_DD_FLAG_TIMING       4  /* record per-kernel CUDA events (see pinn_dd_kernel_times) */
+#define PINN_DD_FLAG_PEER_STORES 16  /* remote twins move by stores into the neighbours' memory inside
+                                        the fused launch (pinn_dd_ipc_export / pinn_dd_connect_peers) */
 #define PINN_DD_FLAG_TF32         8  /* width-80 nets: hidden-layer contractions on the tensor cores
                                         (tcgen05.mma kind::tf32, single-pass TF32 products, FP32
                                         accumulation; looser tolerance, DESIGN.md 6 / 11).  Compiled
@@ -259,6 +261,26 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host);
    (ncclGroupStart / ncclSend / ncclRecv / ncclGroupEnd on desc->stream).
    Collective over the peers: they must all call it. */
 pinn_dd_status pinn_dd_exchange(pinn_dd* h);
+
+/* Peer-store transport (PINN_DD_FLAG_PEER_STORES; Algorithm 1 lines 244-265 fused
+   into the step's persistent launch).  Every rank exports its exchange
+   region -- per-peer arrival counters (uint64) and payload rows -- as a CUDA IPC
+   handle (64 bytes) of the allocation holding it plus byte offsets, the ranks
+   trade them (e.g. an all-gather), and each connects to its peers.  Then
+   pinn_dd_step runs ONE persistent launch (+ K5) per iteration: payload chunks
+   store every cut-edge row straight into the neighbour's receive slot (slot =
+   step parity) and release-add the row counts to its arrival counter; the
+   interface loss chunks acquire-wait for all peers' rows of the step while the
+   interior chunks compute.  Every rank must step in lock-step. */
+pinn_dd_status pinn_dd_ipc_export(pinn_dd* h, void* handle64, int64_t* flags_offset, int64_t* rows_offset);
+/* For peer i of the exchange plan: handles[i] (64 bytes), the offsets of its
+   pinn_dd_ipc_export, peer_row[i] = the peer's first received row from this rank
+   (its peer_recv_row), peer_nrecv[i] = the peer's n_recv (slot stride),
+   peer_flag[i] = this rank's index among the peer's peers.  A peer whose rank is
+   desc->rank is this handle itself (loop-back; its handle is not opened). */
+pinn_dd_status pinn_dd_connect_peers(pinn_dd* h, const void* handles, const int64_t* flags_offset,
+                                     const int64_t* rows_offset, const int64_t* peer_row,
+                                     const int64_t* peer_nrecv, const int32_t* peer_flag);
 
 /* A fresh 128-byte ncclUniqueId (host) for desc->nccl_id (PINN_DD_ENCCL if NCCL
    cannot be loaded). */

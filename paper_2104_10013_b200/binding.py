@@ -25,7 +25,7 @@ OK, EINVAL, EUNSUPPORTED, ECUDA, ENCCL, ENONFINITE, EPROTOCOL = range(7)
 METHODS = {"pinn": 0, "cpinn": 1, "xpinn": 2, "hybrid": 3}
 PDES = {"burgers": 0, "poisson": 1, "heat": 2, "ns": 3, "heat_inv": 4}
 ACTS = {"tanh": 0, "sin": 1, "cos": 2}
-FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING, FLAG_TF32 = 1, 2, 4, 8
+FLAG_GRAPH, FLAG_GLOBAL_STASH, FLAG_TIMING, FLAG_TF32, FLAG_PEER_STORES = 1, 2, 4, 8, 16
 GEOM_NONE, GEOM_BOXES, GEOM_VORONOI = 0, 1, 2
 PREDICT_STITCHED, PREDICT_OWNER = 0, 1
 STATUS_J, STATUS_GRAD, STATUS_SLOPE, STATUS_SLOPE_ZERO = 1, 2, 4, 8
@@ -34,7 +34,7 @@ EXPORTS = [
     "pinn_dd_n_params", "pinn_dd_workspace_size", "pinn_dd_create", "pinn_dd_interface_payload",
     "pinn_dd_payload_buffer", "pinn_dd_loss_grad", "pinn_dd_loss_grad_interior", "pinn_dd_loss_grad_interface",
     "pinn_dd_adam", "pinn_dd_step", "pinn_dd_predict", "pinn_dd_predict_owners", "pinn_dd_exchange",
-    "pinn_dd_nccl_unique_id",
+    "pinn_dd_nccl_unique_id", "pinn_dd_ipc_export", "pinn_dd_connect_peers",
     "pinn_dd_get_params", "pinn_dd_set_params", "pinn_dd_get_step", "pinn_dd_kernel_times",
     "pinn_dd_plan_info", "pinn_dd_step_fused", "pinn_dd_read_loss", "pinn_dd_debug_buffer", "pinn_dd_destroy", "pinn_dd_last_error",
 ]
@@ -105,6 +105,9 @@ def load_library(path: str = LIB_PATH):
     lib.pinn_dd_predict_owners.argtypes = [vp, vp, vp, i64, vp]
     lib.pinn_dd_exchange.argtypes = [vp]
     lib.pinn_dd_nccl_unique_id.argtypes = [vp]
+    lib.pinn_dd_ipc_export.argtypes = [vp, vp, C.POINTER(i64), C.POINTER(i64)]
+    lib.pinn_dd_connect_peers.argtypes = [vp, vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
+                                          C.POINTER(i32)]
     lib.pinn_dd_get_params.argtypes = [vp, i32, i32, vp]
     lib.pinn_dd_set_params.argtypes = [vp, i32, i32, vp]
     lib.pinn_dd_get_step.argtypes = [vp, i32, C.POINTER(i32)]
@@ -325,9 +328,11 @@ class PinnDD:
     on an internal stream, captured with the rest of the iteration into one
     CUDA graph by pinn_dd_step).  With world > 1, rank 0 draws the NCCL id and
     `group` (a torch.distributed process group, any backend) broadcasts it.
+    transport="peer": the rows are stored straight into the neighbours' memory
+    by the fused launch (CUDA IPC handles traded over `group`).
     loopback=True (single process): edges between different owners are
-    exchanged with this rank itself through NCCL -- the multi-GPU data path
-    validated on one GPU."""
+    exchanged with this rank itself through the chosen transport -- the
+    multi-GPU data path validated on one GPU."""
 
     def __init__(self, prob, local: Optional[Sequence[int]] = None, owner: Optional[Sequence[int]] = None,
                  rank: int = 0, device=None, flags: int = FLAG_GRAPH, hparams: Optional[Sequence] = None,
@@ -356,7 +361,11 @@ class PinnDD:
                                                mask=self.mask.data_ptr(), init_params=self.init_params.data_ptr()),
                                   self.stream.cuda_stream, flags, hparams, norm_counts)
         nccl_id = None
-        if transport == "nccl":
+        if transport == "peer":
+            flags |= FLAG_PEER_STORES
+            d.flags = flags
+            d.rank, d.world = (rank, 1) if loopback else (rank, world)
+        elif transport == "nccl":
             if world > 1:
                 import torch.distributed as dist
                 obj = [nccl_unique_id() if rank == 0 else None]
@@ -370,6 +379,7 @@ class PinnDD:
         elif transport is not None:
             raise ValueError(f"unknown transport {transport!r}")
         self.transport = transport
+        self.rank = rank
         self.desc = d
         nbytes = C.c_size_t(0)
         self._check(self.lib.pinn_dd_workspace_size(C.byref(d), C.byref(nbytes)), None)
@@ -385,6 +395,47 @@ class PinnDD:
         assert off % 4 == 0
         self.payload = self.workspace[off: off + 4 * self.n_rows * self.n_fields].view(torch.float32).view(
             self.n_rows, self.n_fields)
+        if transport == "peer":
+            self._connect_peers(group, world, loopback)
+
+    def _connect_peers(self, group, world, loopback):
+        """Trade the exchange regions (CUDA IPC) and connect every peer of the plan."""
+        handle = (C.c_char * 64)()
+        foff, roff = C.c_int64(), C.c_int64()
+        self._check(self.lib.pinn_dd_ipc_export(self.h, handle, C.byref(foff), C.byref(roff)))
+        plan = self.table.plan
+        peers = sorted(set(plan.send) | set(plan.recv))
+        mine = dict(rank=self.rank, handle=bytes(handle), foff=foff.value, roff=roff.value, peers=peers,
+                    recv={p: plan.recv.get(p, (0, 0))[0] for p in peers}, n_recv=plan.n_recv)
+        if loopback or world == 1:
+            allinfo = {self.rank: mine}
+        else:
+            import torch.distributed as dist
+            got = [None] * world
+            dist.all_gather_object(got, mine, group=group)
+            allinfo = {g["rank"]: g for g in got}
+        n = len(peers)
+        hs = (C.c_char * (64 * max(1, n)))()
+        fo, ro, prow, pn = (C.c_int64 * max(1, n))(), (C.c_int64 * max(1, n))(), (C.c_int64 * max(1, n))(), \
+            (C.c_int64 * max(1, n))()
+        pf = (C.c_int32 * max(1, n))()
+        for i, p in enumerate(peers):
+            o = allinfo[p]
+            C.memmove(C.addressof(hs) + 64 * i, o["handle"], 64)
+            fo[i], ro[i] = o["foff"], o["roff"]
+            prow[i] = o["recv"][self.rank]
+            pn[i] = o["n_recv"]
+            pf[i] = o["peers"].index(self.rank)
+        st = self.lib.pinn_dd_connect_peers(self.h, hs, fo, ro, prow, pn, pf)
+        if not (loopback or world == 1):
+            # every rank connected, or every rank raises (no rank left waiting in a step)
+            import torch.distributed as dist
+            dev = self.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+            ok = torch.tensor([1 if st == OK else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if st == OK and int(ok.item()) == 0:
+                raise PinnDDError(EPROTOCOL, "peer stores: another rank failed to connect")
+        self._check(st)
 
     # ------------------------------------------------------------------
     def _check(self, status, h="self"):

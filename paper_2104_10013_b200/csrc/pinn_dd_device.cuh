@@ -124,7 +124,7 @@ struct KCfg {
   // accumulator in global memory, to coalesce the per-tile read-modify-write
   static constexpr int SCR = (S > 1 || !DW_SMEM) ? SCR1 : 0;
   static constexpr int oAcc = al4(oDw + SCR);              // per-chunk gradient accumulator
-  static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 4);   // + tmem address slot
+  static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 12);  // + peer row counts [8], tmem slot, s_next
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= SMEM_CAP, "shared memory budget");
   static_assert(NBLK * S <= T, "dW blocks per CTA");
@@ -475,6 +475,34 @@ __device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
   return v;
 }
 
+// Peer-store exchange of the fused step (PINN_DD_FLAG_PEER_STORES, Algorithm 1
+// green stage inside the launch): payload chunks store the rows of
+// cut edges straight into the neighbour GPU's receive slot (CUDA-IPC-mapped,
+// over NVLink) and release-add the row count to its arrival counter; interface
+// loss chunks acquire-wait for every peer's rows of this step.  Receive slots
+// alternate by step parity (a neighbour can be one step ahead of our reads).
+constexpr int kMaxPeers = 8;
+struct PeerX {
+  int n;                                      // peers (0: off)
+  int64_t send_off[kMaxPeers + 1];            // send-slot ranges of the peers (psend indices)
+  float* dst[kMaxPeers];                      // peer's receive slot 0, first row of ours
+  int64_t slot_stride[kMaxPeers];             // floats from the peer's slot 0 to its slot 1
+  unsigned long long* peer_flag[kMaxPeers];   // peer's arrival counter for our rows
+  const unsigned long long* my_flag;          // [n] arrivals here, per peer (cumulative)
+  int64_t expect[kMaxPeers];                  // rows per step from each peer
+  int64_t n_recv;                             // rows of one receive slot here
+  int* step;                                  // steps completed (parity, expected arrivals)
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+
 struct KArgs {
   const float* coords;      // [2][n_points]
   const float* target;      // [DO][n_points]
@@ -499,6 +527,7 @@ struct KArgs {
   float* payload;           // [rows][NF]
   const int32_t* psend;     // [n_points] row of the point in the send buffer, -1 = not sent (nullptr: no peers)
   float* sendbuf;           // [n_send][NF] payload rows of cut edges, in the peers' receive order
+  PeerX px;                 // peer-store exchange of the fused step (px.n == 0: off)
   float* gstash;            // global stash fallback (nullptr = TMEM)
   PdeConst pc;
   int method;               // 0 pinn, 1 cpinn, 2 xpinn, 3 hybrid (per-edge choice in pinfo bit 2)

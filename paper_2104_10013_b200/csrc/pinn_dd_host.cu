@@ -248,6 +248,12 @@ struct pinn_dd {
   cudaEvent_t xfork = nullptr, xjoin = nullptr;
   float* sendbuf = nullptr;
   int32_t* psend = nullptr;
+  // peer-store transport (PINN_DD_FLAG_PEER_STORES)
+  bool peers_connected = false;
+  PeerX px{};
+  unsigned long long* xflags = nullptr;   // [kMaxPeers] arrivals here, per peer
+  int* xstep = nullptr;                    // fused steps completed
+  std::vector<void*> ipc_open;             // peer allocations opened with cudaIpcOpenMemHandle
   // Eq. (4) geometry
   std::vector<float> geo;               // boxes [n_geo][4] or seeds [n_geo][2]
   std::vector<float> poly;              // [n_poly][2]
@@ -370,7 +376,8 @@ struct Carve {
 struct Layout {
   size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ord1,
       sched, ch2, subch,
-      tstep, done, sflag, loss, packmap, slopep, sendbuf, psend, dgeo, dpoly, dgeoloc, gstash, total;
+      tstep, done, sflag, loss, packmap, slopep, sendbuf, psend, dgeo, dpoly, dgeoloc, xflags, xstep, gstash,
+      total;
 };
 
 // validation + planning shared by workspace_size and create
@@ -483,6 +490,10 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   }
   if (d->nccl_id && (d->world < 1 || d->rank < 0 || d->rank >= d->world))
     return fail(h, PINN_DD_EINVAL, "rank %d / world %d", d->rank, d->world);
+  if (d->flags & PINN_DD_FLAG_PEER_STORES) {
+    if (d->nccl_id) return fail(h, PINN_DD_EINVAL, "PINN_DD_FLAG_PEER_STORES and nccl_id are exclusive");
+    if (d->n_peers > kMaxPeers) return fail(h, PINN_DD_EUNSUPPORTED, "peer stores: at most %d peers", kMaxPeers);
+  }
   // Eq. (4) geometry
   if (d->geometry < 0 || d->geometry > 2) return fail(h, PINN_DD_EINVAL, "bad geometry %d", d->geometry);
   if (d->geometry != PINN_DD_GEOM_NONE) {
@@ -520,7 +531,9 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->scratch = c.take<float>(ns * pstride);
   L->partial = c.take<float>(size_t(n1) * pstride);
   L->ploss = c.take<float>(size_t(n1) * 4);
-  L->payload = c.take<float>((npt + size_t(d->n_recv) + 1) * nf);
+  // peer stores alternate two receive slots by step parity
+  const size_t nslots = (d->flags & PINN_DD_FLAG_PEER_STORES) ? 2 : 1;
+  L->payload = c.take<float>((npt + nslots * size_t(d->n_recv) + 1) * nf);
   L->pinfo = c.take<int32_t>(npt + 1);
   L->pinv = c.take<float>(npt + 1);
   L->ptwin = c.take<int32_t>(npt + 1);
@@ -545,6 +558,8 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->dgeo = c.take<float>(size_t(ngeo) * 4 + 4);
   L->dpoly = c.take<float>(size_t(d->geometry == PINN_DD_GEOM_VORONOI ? d->n_poly : 0) * 2 + 2);
   L->dgeoloc = c.take<int32_t>(size_t(ngeo) + 1);
+  L->xflags = c.take<unsigned long long>(kMaxPeers);
+  L->xstep = c.take<int32_t>(1);
   L->gstash = (d->flags & PINN_DD_FLAG_GLOBAL_STASH)
                   ? c.take<float>(size_t(grid1) * d->n_hidden * kA * ops->threads)
                   : c.off;
@@ -595,6 +610,8 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.payload = h->payload;
   a.psend = h->send_rows.empty() ? nullptr : h->psend;
   a.sendbuf = h->sendbuf;
+  a.px = h->px;
+  a.px.n = 0;   // only the fused step stores into peers (launch_fused)
   a.gstash = (d.flags & PINN_DD_FLAG_GLOBAL_STASH) ? h->gstash : nullptr;
   a.pc.pde = d.pde;
   a.pc.nu = d.nu;
@@ -714,16 +731,19 @@ pinn_dd_status launch_fused(pinn_dd* h) {
   KArgs a = make_kargs(h, false);
   a.chunks2 = h->chunks2;
   a.n_chunks2 = h->n_chunks2;
+  if (h->peers_connected) a.px = h->px;
   h->ops->kf(a, std::min(h->grid1, a.n_chunks + a.n_chunks2), h->ops->smem, h->stream);
   ++h->launches;
   CK(h, cudaGetLastError());
   return PINN_DD_OK;
 }
 
-bool remote(const pinn_dd* h) { return !h->peer_rank.empty(); }
+// remote twins exchanged by NCCL (or the caller); peer stores run in the fused launch
+bool remote(const pinn_dd* h) { return !h->peer_rank.empty() && !h->peers_connected; }
 
 bool use_fused(const pinn_dd* h) {
   static const bool off = std::getenv("PINN_DD_NO_FUSED_STEP") != nullptr;   // development A/B knob
+  if (h->peers_connected) return true;
   return h->ops->kf && h->n_chunks2 > 0 && h->d.n_recv == 0 && !remote(h) && !off;
 }
 
@@ -942,6 +962,8 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->dgeo = reinterpret_cast<float*>(base + L.dgeo);
   h->dpoly = reinterpret_cast<float*>(base + L.dpoly);
   h->dgeo_local = reinterpret_cast<int32_t*>(base + L.dgeoloc);
+  h->xflags = reinterpret_cast<unsigned long long*>(base + L.xflags);
+  h->xstep = reinterpret_cast<int*>(base + L.xstep);
 
   // ---- per-point classification and 1/N (Eq. 3/5/6; per-edge mean, Z2)
   const int64_t np = d->n_points;
@@ -1077,7 +1099,12 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   CKC(cudaMemsetAsync(h->m, 0, pbytes, st));
   CKC(cudaMemsetAsync(h->v, 0, pbytes, st));
   CKC(cudaMemsetAsync(h->grad, 0, pbytes, st));
-  CKC(cudaMemsetAsync(h->payload, 0, (size_t(np) + d->n_recv + 1) * h->nf * sizeof(float), st));
+  {
+    const size_t nslots = (d->flags & PINN_DD_FLAG_PEER_STORES) ? 2 : 1;
+    CKC(cudaMemsetAsync(h->payload, 0, (size_t(np) + nslots * d->n_recv + 1) * h->nf * sizeof(float), st));
+  }
+  CKC(cudaMemsetAsync(h->xflags, 0, kMaxPeers * sizeof(unsigned long long), st));
+  CKC(cudaMemsetAsync(h->xstep, 0, sizeof(int), st));
   // K1 never writes a partial's padding slots; K5a sums every index, so they start (and stay) 0
   CKC(cudaMemsetAsync(h->partial, 0, size_t(h->n_chunks1) * h->pstride * sizeof(float), st));
   CKC(cudaMemcpyAsync(h->pinfo, pinfo.data(), pinfo.size() * 4, cudaMemcpyHostToDevice, st));
@@ -1250,8 +1277,9 @@ pinn_dd_status pinn_dd_step(pinn_dd* h, int32_t n_iters, float* loss_host) {
   if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
   if (remote(h) && !h->comm)
     return fail(h, PINN_DD_EPROTOCOL,
-                "pinn_dd_step with remote twins (n_recv = %lld) needs the NCCL transport (desc nccl_id); "
-                "else use the phased calls",
+                "pinn_dd_step with remote twins (n_recv = %lld) needs a transport: NCCL (desc nccl_id) or "
+                "connected peer stores (PINN_DD_FLAG_PEER_STORES + pinn_dd_connect_peers); else use the "
+                "phased calls",
                 (long long)h->d.n_recv);
   if (n_iters < 0) return fail(h, PINN_DD_EINVAL, "n_iters < 0");
   const bool timed = (h->d.flags & PINN_DD_FLAG_TIMING) != 0;
@@ -1387,6 +1415,76 @@ pinn_dd_status pinn_dd_exchange(pinn_dd* h) {
   return nccl_group(h, h->stream);
 }
 
+pinn_dd_status pinn_dd_ipc_export(pinn_dd* h, void* handle64, int64_t* flags_offset, int64_t* rows_offset) {
+  if (!h || !handle64 || !flags_offset || !rows_offset) return fail(h, PINN_DD_EINVAL, "bad ipc_export arguments");
+  if (!(h->d.flags & PINN_DD_FLAG_PEER_STORES)) return fail(h, PINN_DD_EINVAL, "handle without PINN_DD_FLAG_PEER_STORES");
+  cudaIpcMemHandle_t ih;
+  CK(h, cudaIpcGetMemHandle(&ih, h->payload));
+  // offsets inside the allocation the handle maps: its base via the driver API
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange get_range = [] {
+    void* lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libcuda.so.1", RTLD_NOW);
+    return lib ? reinterpret_cast<GetRange>(dlsym(lib, "cuMemGetAddressRange_v2")) : nullptr;
+  }();
+  if (!get_range) return fail(h, PINN_DD_ECUDA, "cuMemGetAddressRange_v2 unavailable");
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (get_range(&b, &sz, reinterpret_cast<unsigned long long>(h->payload)) != 0)
+    return fail(h, PINN_DD_ECUDA, "cuMemGetAddressRange_v2 failed");
+  std::memcpy(handle64, &ih, sizeof ih);
+  *flags_offset = int64_t(reinterpret_cast<uintptr_t>(h->xflags) - b);
+  *rows_offset = int64_t(reinterpret_cast<uintptr_t>(h->payload) - b);
+  return PINN_DD_OK;
+}
+
+pinn_dd_status pinn_dd_connect_peers(pinn_dd* h, const void* handles, const int64_t* flags_offset,
+                                     const int64_t* rows_offset, const int64_t* peer_row, const int64_t* peer_nrecv,
+                                     const int32_t* peer_flag) {
+  if (!h) return fail(nullptr, PINN_DD_EINVAL, "handle is NULL");
+  if (!(h->d.flags & PINN_DD_FLAG_PEER_STORES)) return fail(h, PINN_DD_EINVAL, "handle without PINN_DD_FLAG_PEER_STORES");
+  const int n = int(h->peer_rank.size());
+  if (n == 0) return PINN_DD_OK;
+  if (!handles || !flags_offset || !rows_offset || !peer_row || !peer_nrecv || !peer_flag)
+    return fail(h, PINN_DD_EINVAL, "bad connect_peers arguments");
+  if (h->ops->kf == nullptr || h->n_chunks2 == 0)
+    return fail(h, PINN_DD_EUNSUPPORTED, "peer stores need the fused step (interface points on this handle)");
+  PeerX px{};
+  px.n = n;
+  for (int i = 0; i <= n; ++i) px.send_off[i] = h->peer_send_off[i];
+  for (int i = 0; i < n; ++i) {
+    char* base;
+    if (h->peer_rank[i] == h->d.rank) {
+      base = nullptr;   // loop-back: this handle's own region
+    } else {
+      cudaIpcMemHandle_t ih;
+      std::memcpy(&ih, static_cast<const char*>(handles) + 64 * size_t(i), sizeof ih);
+      void* p = nullptr;
+      CK(h, cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_open.push_back(p);
+      base = static_cast<char*>(p);
+    }
+    float* rows = base ? reinterpret_cast<float*>(base + rows_offset[i]) : h->payload;
+    unsigned long long* flags = base ? reinterpret_cast<unsigned long long*>(base + flags_offset[i]) : h->xflags;
+    if (peer_flag[i] < 0 || peer_flag[i] >= kMaxPeers || peer_nrecv[i] < 0 || peer_row[i] < 0)
+      return fail(h, PINN_DD_EPROTOCOL, "peer %d: bad row / flag description", i);
+    px.dst[i] = rows + size_t(peer_row[i]) * h->nf;
+    px.slot_stride[i] = peer_nrecv[i] * h->nf;
+    px.peer_flag[i] = flags + peer_flag[i];
+    px.expect[i] = h->peer_recv_n[i];
+  }
+  px.my_flag = h->xflags;
+  px.n_recv = h->d.n_recv;
+  px.step = h->xstep;
+  h->px = px;
+  h->peers_connected = true;
+  if (h->gexec) {   // the captured step graph predates the transport
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  return PINN_DD_OK;
+}
+
 pinn_dd_status pinn_dd_nccl_unique_id(void* id128) {
   if (!id128) return fail(nullptr, PINN_DD_EINVAL, "id128 is NULL");
   const Nccl& N = nccl();
@@ -1440,6 +1538,7 @@ void pinn_dd_destroy(pinn_dd* h) {
     if (e) cudaEventDestroy(e);
   if (h->gstream) cudaStreamDestroy(h->gstream);
   if (h->comm) nccl().CommDestroy(h->comm);
+  for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
   if (h->cstream) cudaStreamDestroy(h->cstream);
   if (h->xfork) cudaEventDestroy(h->xfork);
   if (h->xjoin) cudaEventDestroy(h->xjoin);

@@ -335,7 +335,8 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
 // epilogue of one point (K2): u(x_I) and f.n (cPINN) or F (XPINN) into its
 // payload row (Algorithm 1)
 template <int DO>
-__device__ __forceinline__ void point_payload(const KArgs& a, int64_t gp, float x, float y, const float4* U) {
+__device__ __forceinline__ void point_payload(const KArgs& a, int64_t gp, float x, float y, const float4* U,
+                                              int step = 0, int* xcount = nullptr) {
   constexpr int NF = DO + (DO == 3 ? 3 : 1);
   float r[3];
   float dr[3][DO][4];
@@ -351,14 +352,61 @@ __device__ __forceinline__ void point_payload(const KArgs& a, int64_t gp, float 
 #pragma unroll
   for (int o = 0; o < DO; ++o) q[o] = U[o].x;
   for (int e = 0; e < ne; ++e) q[DO + e] = r[e];
-  // a point of a cut edge also goes to the send buffer of its neighbour's rank
-  // (the exchange reads it right after this kernel, Algorithm 1)
+  // a point of a cut edge also goes to its neighbour's rank (Algorithm 1 lines
+  // 244-252): into the send buffer (the NCCL exchange reads it after this
+  // kernel), or -- peer stores, fused step -- straight into the neighbour's
+  // receive slot of this step's parity, counted per peer in xcount
   const int ss = a.psend ? a.psend[gp] : -1;
   if (ss >= 0) {
-    float* w = a.sendbuf + size_t(ss) * NF;
+    float* w;
+    if (xcount) {
+      int i = 0;
+      while (i + 1 < a.px.n && ss >= a.px.send_off[i + 1]) ++i;
+      w = a.px.dst[i] + (step & 1) * a.px.slot_stride[i] + (ss - a.px.send_off[i]) * NF;
+      atomicAdd(xcount + i, 1);
+    } else {
+      w = a.sendbuf + size_t(ss) * NF;
+    }
 #pragma unroll
     for (int o = 0; o < DO; ++o) w[o] = U[o].x;
     for (int e = 0; e < ne; ++e) w[DO + e] = r[e];
+  }
+}
+
+// the peer-store protocol of the fused step (PeerX): after a payload chunk,
+// release this chunk's row counts to the peers' arrival counters (the CTA
+// barrier orders every thread's row stores before thread 0's release)
+__device__ __forceinline__ void publish_peer_rows(const KArgs& a, int* xcount) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int i = 0; i < a.px.n; ++i)
+      if (xcount[i]) {
+        red_release_sys_add(a.px.peer_flag[i], (unsigned long long)xcount[i]);
+        xcount[i] = 0;
+      }
+  }
+}
+// before an interface loss chunk: every local payload chunk and every peer's
+// rows of this step have arrived
+// A wait that has not ended after ~20 s (a peer that never runs its step)
+// traps: the launch fails with an error instead of hanging the device.
+__device__ __forceinline__ void spin_guard(long long t0) {
+  if (clock64() - t0 > 40000000000LL) __trap();
+}
+__device__ __forceinline__ void wait_payload(const KArgs& a, int n_pay, int step) {
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    while (ld_acquire_gpu(a.sched + 4) < n_pay) {
+      __nanosleep(64);
+      spin_guard(t0);
+    }
+    for (int i = 0; i < a.px.n; ++i) {
+      const unsigned long long want = (unsigned long long)(step + 1) * (unsigned long long)a.px.expect[i];
+      while (ld_acquire_sys_u64(a.px.my_flag + i) < want) {
+        __nanosleep(64);
+        spin_guard(t0);
+      }
+    }
   }
 }
 
@@ -366,7 +414,7 @@ __device__ __forceinline__ void point_payload(const KArgs& a, int64_t gp, float 
 // MSE_uavg, MSE_if partials) and the adjoint seeds Ub = dJ/dU (a8)
 template <int DO>
 __device__ __forceinline__ void point_adjoint(const KArgs& a, int64_t gp, float x, float y, float4 lw,
-                                              const float4* U, float4* Ub, float* lsum) {
+                                              const float4* U, float4* Ub, float* lsum, int64_t roff = 0) {
   constexpr int NF = DO + (DO == 3 ? 3 : 1);
   const int info = a.pinfo[gp];
   const int kind = info & 3;
@@ -398,7 +446,9 @@ __device__ __forceinline__ void point_adjoint(const KArgs& a, int64_t gp, float 
     }
   } else {
     // interface point: neighbour payload is a constant
-    const float* q = a.payload + size_t(a.ptwin[gp]) * NF;   // read via L2 (__ldcg): rows written by other CTAs
+    int64_t tw = a.ptwin[gp];
+    if (tw >= a.n_points) tw += roff;                          // received rows: this step's slot
+    const float* q = a.payload + size_t(tw) * NF;   // read via L2 (__ldcg): rows written by other CTAs / GPUs
 #pragma unroll
     for (int o = 0; o < DO; ++o) {
       const float d = U[o].x - __ldcg(q + o);   // u_q - {{u}} = d / 2  (Z1)
@@ -491,8 +541,15 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   // waits until every payload chunk is done (all CTAs are resident and payload
   // chunks are handed out first, so the wait always ends).
   int& s_next = *reinterpret_cast<int*>(sm + C::TOTAL - 3);   // next chunk index (dynamic smem, after tslot)
+  int* xcount = reinterpret_cast<int*>(sm + C::TOTAL - 12);    // [kMaxPeers] peer rows of a payload chunk
   int cur_sub = -1;
   const int n_pay = MODE == 2 ? a.n_chunks2 : 0;
+  // peer-store exchange of the fused step: this launch's step index (receive
+  // slot parity, expected arrivals) and per-peer row counts of a payload chunk
+  const bool px = MODE == 2 && a.px.n > 0;
+  const int xstep = px ? *reinterpret_cast<volatile int*>(a.px.step) : 0;
+  const int64_t roff = px ? int64_t(xstep & 1) * a.px.n_recv : 0;
+  if (tid < kMaxPeers) xcount[tid] = 0;
 #pragma unroll 1
   for (;;) {
     if (tid == 0) s_next = atomicAdd(a.sched, 1);
@@ -504,10 +561,8 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (a.order ? a.order[li] : li);
     const Chunk ch = (MODE == 2 && pay) ? a.chunks2[c] : a.chunks[c];
     if (MODE == 2 && !pay && ch.pad) {
-      // interface loss chunk: acquire the completed payload rows
-      if (tid == 0) {
-        while (ld_acquire_gpu(a.sched + 4) < n_pay) __nanosleep(64);
-      }
+      // interface loss chunk: acquire the completed payload rows (local, and the peers')
+      wait_payload(a, n_pay, xstep);
       cta_sync();
     }
     if (ch.sub != cur_sub) {
@@ -625,7 +680,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             float4 U[DO];
 #pragma unroll
             for (int o = 0; o < DO; ++o) U[o] = sU[p * DO + o];
-            point_payload<DO>(a, p0 + p, sX[p], sY[p], U);
+            point_payload<DO>(a, p0 + p, sX[p], sY[p], U, xstep, px ? xcount : nullptr);
           }
           continue;
         } else {
@@ -636,7 +691,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
               U[o] = sU[p * DO + o];
               Ub[o] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             }
-            if (p < np) point_adjoint<DO>(a, p0 + p, sX[p], sY[p], lw, U, Ub, lsum);
+            if (p < np) point_adjoint<DO>(a, p0 + p, sX[p], sY[p], lw, U, Ub, lsum, roff);
 #pragma unroll
             for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
           }
@@ -807,6 +862,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     if (MODE == 2 && pay) {
       // publish this payload chunk (release: all its rows are written)
       cta_sync();
+      if (px) publish_peer_rows(a, xcount);
       if (tid == 0) {
         __threadfence();
         atomicAdd(a.sched + 4, 1);
@@ -826,6 +882,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
       a.sched[0] = 0;
       a.sched[1] = 0;
       if (MODE == 2) a.sched[4] = 0;
+      if (px) *a.px.step = xstep + 1;
       __threadfence();
     }
   }

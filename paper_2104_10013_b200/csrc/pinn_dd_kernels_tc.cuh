@@ -229,7 +229,7 @@ struct TcCfg {
   static constexpr int oX = al4(oSl + NH);                   // [2][P]
   static constexpr int oU = oX + 2 * P;                      // [P][DO] float4
   static constexpr int oMisc = oU + 4 * P * DO;              // loss scratch [8][4], mbarrier, tmem slot, s_next
-  static constexpr int TOTAL = oMisc + 32 + 8;   // loss scratch, 2 mbarriers, tmem slot, s_next
+  static constexpr int TOTAL = oMisc + 32 + 16;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget of the tensor-core kernel");
   static_assert((oH * 4) % 1024 == 0 && (oZ * 4) % 1024 == 0 && (WOPER * 4) % 1024 == 0, "operand alignment");
@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   uint64_t* mbar2 = reinterpret_cast<uint64_t*>(sm + C::oMisc + 34);   // dW MMAs
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::oMisc + 36);
   int* s_next = reinterpret_cast<int*>(sm + C::oMisc + 37);
+  int* xcount = reinterpret_cast<int*>(sm + C::oMisc + 38);    // [kMaxPeers] peer rows of a payload chunk
   const float m1 = a.m1, m2 = a.m2;
   const uint32_t aH = smem_u32(sH), aZ = smem_u32(sZ), aW = smem_u32(sW);
 
@@ -310,6 +311,12 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
 
   int cur_sub = -1;
   const int n_pay = MODE == 2 ? a.n_chunks2 : 0;
+  // peer-store exchange of the fused step: this launch's step index (receive
+  // slot parity, expected arrivals) and per-peer row counts of a payload chunk
+  const bool px = MODE == 2 && a.px.n > 0;
+  const int xstep = px ? *reinterpret_cast<volatile int*>(a.px.step) : 0;
+  const int64_t roff = px ? int64_t(xstep & 1) * a.px.n_recv : 0;
+  if (tid < kMaxPeers) xcount[tid] = 0;
 #pragma unroll 1
   for (;;) {
     if (tid == 0) *s_next = atomicAdd(a.sched, 1);
@@ -321,9 +328,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (a.order ? a.order[li] : li);
     const Chunk ch = (MODE == 2 && pay) ? a.chunks2[c] : a.chunks[c];
     if (MODE == 2 && !pay && ch.pad) {
-      if (tid == 0) {
-        while (ld_acquire_gpu(a.sched + 4) < n_pay) __nanosleep(64);
-      }
+      wait_payload(a, n_pay, xstep);   // local payload chunks and the peers' rows
       cta_sync();
     }
     if (ch.sub != cur_sub) {
@@ -432,7 +437,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             float4 U[DO];
 #pragma unroll
             for (int o = 0; o < DO; ++o) U[o] = sU[p * DO + o];
-            point_payload<DO>(a, p0 + p, sX[p], sY[p], U);
+            point_payload<DO>(a, p0 + p, sX[p], sY[p], U, xstep, px ? xcount : nullptr);
           }
           continue;
         } else {
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
               U[o] = sU[p * DO + o];
               Ub[o] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             }
-            if (p < np) point_adjoint<DO>(a, p0 + p, sX[p], sY[p], lw, U, Ub, lsum);
+            if (p < np) point_adjoint<DO>(a, p0 + p, sX[p], sY[p], lw, U, Ub, lsum, roff);
 #pragma unroll
             for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
           }
@@ -633,6 +638,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     }
     if (MODE == 2 && pay) {
       cta_sync();
+      if (px) publish_peer_rows(a, xcount);
       if (tid == 0) {
         __threadfence();
         atomicAdd(a.sched + 4, 1);
@@ -646,6 +652,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       a.sched[0] = 0;
       a.sched[1] = 0;
       if (MODE == 2) a.sched[4] = 0;
+      if (px) *a.px.step = xstep + 1;
       __threadfence();
     }
   }

@@ -186,3 +186,42 @@ def test_predict_library_classification_voronoi():
             ref += w[:, None] * onet.forward(th[q], prob.sizes, Xt, prob.act(q), prob.slope_n).numpy()
     np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-5)
     m.close()
+
+
+# --------------------------------------------------------------------------
+# peer-store transport: the exchange inside the fused persistent launch
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg,kw,blocks,flags", [
+    ("C2", dict(method="xpinn", n_f=500, n_i=25, n_u=20), 2, 0),
+    ("C2", dict(method="cpinn", n_f=500, n_i=25, n_u=20), 8, 0),
+    ("C3", dict(method="hybrid", gpus=8, n_f=500, n_i=30, n_u=40), 8, 0),
+    ("C4", dict(method="xpinn", n_f=300, n_i=20, n_u=16), 4, 0),
+    ("C4", dict(method="xpinn", n_f=300, n_i=20, n_u=16), 4, 8),          # FLAG_TF32 kernel
+    ("C5", dict(scale=0.05, n_i=24, n_u=40), 2, 0),
+])
+def test_peer_store_loopback_step_equals_local_step(cfg, kw, blocks, flags):
+    """pinn_dd_step with PINN_DD_FLAG_PEER_STORES: ONE persistent launch per
+    iteration whose payload chunks store the cut-edge rows into the (here:
+    own) receive slot of the step's parity and release the row counts; the
+    interface loss chunks acquire-wait for them.  Seven iterations (both slot
+    parities, graph-replayed) equal the all-local fused step bitwise; the
+    peer launch count per iteration is the single-GPU one."""
+    import bench
+    from paper_2104_10013_b200.binding import PinnDD, FLAG_GRAPH, FLAG_TIMING
+    prob = perturb_params(make_config(cfg, **kw), scale=0.1)
+    owner = bench.block_owner(prob, blocks) if cfg != "C5" else [q % blocks for q in range(prob.n_sub)]
+    one = PinnDD(prob, device="cuda:0", flags=FLAG_GRAPH | flags)
+    lb = PinnDD(prob, list(range(prob.n_sub)), owner, 0, device="cuda:0", flags=FLAG_GRAPH | FLAG_TIMING | flags,
+                transport="peer", loopback=True)
+    assert lb.table.plan.n_recv > 0 and lb.step_fused
+    a = one.step(7)
+    b = lb.step(7)
+    torch.cuda.synchronize()
+    assert np.array_equal(a, b)
+    for x, y in zip(_state(one), _state(lb)):
+        assert torch.equal(x, y)
+    kt = lb.kernel_times()
+    assert kt[3] == 7 * 3 and kt[4] == 0.0          # fused launch + K5a + K5b, no separate exchange
+    one.close()
+    lb.close()
