@@ -199,10 +199,26 @@ __device__ __forceinline__ void act_derivs(float u, float& s0, float& s1, float&
 // What the reverse sweep needs of a hidden pre-activation jet (z, g1, g2, L):
 // sigma^(k)(s z) for k = 0..3 and (g1, g2, L).  For tanh every sigma^(k) is a
 // polynomial in t = tanh(s z), so the stash keeps (t, g1, g2, L) and the
-// reverse pass evaluates no transcendental; sin / cos keep z itself.
+// reverse pass evaluates no transcendental; sin / cos keep the reduced angle
+// of s z (two MUFU ops per evaluation).
+#if PINN_MUFU_SINCOS
+// sin / cos stash the reduced angle r = s z - 2 pi k in [-pi, pi] (the first
+// half of fast_sincos), so every later evaluation -- forward map, reverse
+// adjoint, reverse recompute -- is the two MUFU ops alone: bitwise the values
+// fast_sincos(s z) gives, without repeating the reduction
+__device__ __forceinline__ float reduce_2pi(float x) {
+  const float k = rintf(x * 0.159154943091895f);
+  const float r = fmaf(-k, 6.28318548202514648f, x);
+  return fmaf(-k, -1.7484555314695172e-7f, r);
+}
+#endif
 template <int ACT>
 __device__ __forceinline__ float stash_x(float zx, float s, int act = ACT) {
+#if PINN_MUFU_SINCOS
+  return act_sel<ACT>(act) == 0 ? tanhf(s * zx) : reduce_2pi(s * zx);
+#else
   return act_sel<ACT>(act) == 0 ? tanhf(s * zx) : zx;
+#endif
 }
 // Scaled derivatives of the activation at u = s z from the stash form x:
 // d0 = sigma, c1 = s sigma', p2 = s^2 sigma'', r3 = s^3 sigma^(3).  For tanh
@@ -219,7 +235,17 @@ __device__ __forceinline__ void scaled_derivs(float x, float s, float& d0, float
     r3 = (a * (s * s * s)) * fmaf(-6.0f, a, 4.0f);
   } else {
     float s0, s1, s2, s3;
+#if PINN_MUFU_SINCOS
+    // x = r, the reduced angle (stash_x)
+    const float sn = __sinf(x), cs = __cosf(x);
+    if (act_sel<ACT>(act) == 1) {
+      s0 = sn; s1 = cs; s2 = -sn; s3 = -cs;
+    } else {
+      s0 = cs; s1 = -sn; s2 = -cs; s3 = sn;
+    }
+#else
     act_derivs<ACT>(s * x, s0, s1, s2, s3, act);
+#endif
     d0 = s0;
     c1 = s * s1;
     p2 = (s * s) * s2;

@@ -551,7 +551,7 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->sflag = c.take<int32_t>(ns);
   L->loss = c.take<float>(ns * 8);
   L->packmap = c.take<int32_t>(size_t(pstride));
-  L->slopep = c.take<double>(ns * size_t((pstride + kRB - 1) / kRB) * kMaxHidden);
+  L->slopep = c.take<double>(ns * size_t((pstride + kRW - 1) / kRW) * kMaxHidden);
   L->sendbuf = c.take<float>(size_t(n_send + 1) * nf);
   L->psend = c.take<int32_t>(npt + 1);
   const int ngeo = d->geometry ? d->n_geo : 0;
@@ -642,6 +642,7 @@ RArgs make_rargs(pinn_dd* h, int mode) {
   r.sflag = h->sflag;
   r.slope_part = h->slope_part;
   r.mode = mode;
+  r.nb5a = (h->pstride + kRW - 1) / kRW;
   h->ops->slopetab(r);
   return r;
 }
@@ -675,9 +676,8 @@ pinn_dd_status launch_k1(pinn_dd* h, int part = 0) {
 pinn_dd_status launch_k5(pinn_dd* h, int mode) {
   dim3 g((h->pstride + kRB - 1) / kRB, h->d.n_sub);
   if (mode != 2) {
-    // status bits of this evaluation start at 0 (loss column 5)
-    CK(h, cudaMemsetAsync(h->sflag, 0, size_t(h->d.n_sub) * 4, h->stream));
-    k_reduce<<<g, kRB, 0, h->stream>>>(make_rargs(h, 0));
+    // status bits of this evaluation start at 0 (zeroed at create and by the K5b that published the last ones)
+    k_reduce<<<dim3((h->pstride + kRW - 1) / kRW, h->d.n_sub), kRB, 0, h->stream>>>(make_rargs(h, 0));
     ++h->launches;
     CK(h, cudaGetLastError());
   }
@@ -731,6 +731,11 @@ pinn_dd_status launch_fused(pinn_dd* h) {
   KArgs a = make_kargs(h, false);
   a.chunks2 = h->chunks2;
   a.n_chunks2 = h->n_chunks2;
+  // loss chunks: residual + training chunks (big first), then the interface
+  // chunks, so that no CTA waits on the payload counter while interior work
+  // is left (C5's one-tile chunks interleaved them: 5 % of K1's samples were
+  // the payload wait)
+  a.order = h->order1 + h->n_chunks1;
   if (h->peers_connected) a.px = h->px;
   h->ops->kf(a, std::min(h->grid1, a.n_chunks + a.n_chunks2), h->ops->smem, h->stream);
   ++h->launches;

@@ -933,63 +933,90 @@ struct RArgs {
   double* slope_part;         // [n_sub][gridDim.x][kMaxHidden] per-block slope partials (K5a -> K5b)
   int mode;                   // k_slope_adam: 0 slopes only, 1 slopes + Adam, 2 Adam only
   int n_hidden;               // 0: no slope parameters
+  int nb5a;                   // K5a blocks per subdomain (slope_part stride)
   int offW[kMaxHidden], nW[kMaxHidden], offB[kMaxHidden], nB[kMaxHidden], offA[kMaxHidden];
 };
 
-// K5a: gradient of subdomain q (blockIdx.y) = sum of its chunk partials in
-// chunk order, accumulated in FP64 (the slope identity below is a cancelling
-// dot product of these sums, so their rounding matters).
-// Indices that are not parameters (16-B padding, slope slots) are never
-// written by K1; the partial region is zeroed once at create.
+// K5a: gradient of subdomain q (blockIdx.y) = sum of its chunk partials,
+// accumulated in FP64 (the slope identity below is a cancelling dot product of
+// these sums, so their rounding matters).  A block owns kRW
+// consecutive entries (a lane owns 4: one 512-B float4 row segment per chunk
+// and warp); warp w sums chunks c0 + w, c0 + w + 8, ... with 8 loads in
+// flight, and warp 0 adds the 8 warp sums in warp order -- a fixed order, so
+// the result is bitwise reproducible, with 64 row loads in flight per entry
+// instead of 8 (C3's single subdomain: 105 chunk partials of 7 blocks were a
+// 20 us latency chain).  Indices that are not parameters (16-B padding, slope
+// slots) are never written by K1; the partial region is zeroed once at create.
+constexpr int kRW = 128;   // entries per K5a block
 __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
-  __shared__ double red[kRB / 32];
+  __shared__ double red[kRB / 32][kRW];
   const int q = blockIdx.y;
-  const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * kRB;
-  const int i = i0 + tid;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int i0 = blockIdx.x * kRW;
+  const int i = i0 + 4 * lane;   // this lane's 4 entries (pstride is a multiple of 4)
   const int c0 = r.sub_chunk[q], c1 = r.sub_chunk[q + 1];
   const float* P = r.params + size_t(q) * r.pstride;
-  double g = 0.0;
-  if (i < r.pstride) {
-    // chunk order, 8 loads in flight per thread
-    int c = c0;
-    for (; c + 8 <= c1; c += 8) {
-      float v[8];
+  {
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    if (i < r.pstride) {
+      constexpr int NW = kRB / 32;
+      const float4* src = reinterpret_cast<const float4*>(r.partial + i);
+      const size_t cs = size_t(r.pstride) / 4;   // float4 per partial
+      int c = c0 + w;
+      for (; c + 7 * NW < c1; c += 8 * NW) {
+        float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldcg(r.partial + size_t(c + u) * r.pstride + i);
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + size_t(c + u * NW) * cs);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) g += double(v[u]);
+        for (int u = 0; u < 8; ++u) {
+          g[0] += double(v[u].x); g[1] += double(v[u].y); g[2] += double(v[u].z); g[3] += double(v[u].w);
+        }
+      }
+      for (; c < c1; c += NW) {
+        const float4 v = __ldcg(src + size_t(c) * cs);
+        g[0] += double(v.x); g[1] += double(v.y); g[2] += double(v.z); g[3] += double(v.w);
+      }
     }
-    for (; c < c1; ++c) g += double(__ldcg(r.partial + size_t(c) * r.pstride + i));
-    const float gf = float(g);
-    r.grad[size_t(q) * r.pstride + i] = gf;
-    if (!isfinite(gf)) atomicOr(r.sflag + q, kFlagGrad);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) red[w][4 * lane + e] = g[e];
   }
-  // per-block partial sums of <W^k, dJ/dW^k> + <b^k, dJ/db^k> (fp64, fixed
-  // order, from the FP64 sums above) for the slope identity; K5b combines them
-  // (no cross-block reads of parameters that K5b's Adam updates)
-  for (int k = 0; k < r.n_hidden; ++k) {
-    const int w0 = r.offW[k], w1 = w0 + r.nW[k], b0 = r.offB[k], b1 = b0 + r.nB[k];
-    double* slot = r.slope_part + (size_t(q) * gridDim.x + blockIdx.x) * kMaxHidden + k;
-    const bool hit = (w0 < i0 + kRB && w1 > i0) || (b0 < i0 + kRB && b1 > i0);   // block-uniform
-    if (!hit) {
-      if (tid == 0) *slot = 0.0;
-      continue;
-    }
-    double acc = ((i >= w0 && i < w1) || (i >= b0 && i < b1)) ? double(P[i]) * g : 0.0;
+  __syncthreads();
+  if (w == 0) {
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((tid & 31) == 0) red[tid >> 5] = acc;
-    __syncthreads();
-    if (tid == 0) {
-      double sum = 0.0;
-      for (int w = 0; w < kRB / 32; ++w) sum += red[w];
-      *slot = sum;
+    for (int ww = 0; ww < kRB / 32; ++ww)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) g[e] += red[ww][4 * lane + e];
+    if (i < r.pstride) {
+      float4 gf = make_float4(float(g[0]), float(g[1]), float(g[2]), float(g[3]));
+      *reinterpret_cast<float4*>(r.grad + size_t(q) * r.pstride + i) = gf;
+      if (!isfinite(gf.x) || !isfinite(gf.y) || !isfinite(gf.z) || !isfinite(gf.w)) atomicOr(r.sflag + q, kFlagGrad);
     }
-    __syncthreads();
+    // per-block partial sums of <W^k, dJ/dW^k> + <b^k, dJ/db^k> (fp64, fixed
+    // order, from the FP64 sums above) for the slope identity; K5b combines
+    // them (no cross-block reads of parameters that K5b's Adam updates)
+    for (int k = 0; k < r.n_hidden; ++k) {
+      const int w0 = r.offW[k], w1 = w0 + r.nW[k], b0 = r.offB[k], b1 = b0 + r.nB[k];
+      double* slot = r.slope_part + (size_t(q) * gridDim.x + blockIdx.x) * kMaxHidden + k;
+      const bool hit = (w0 < i0 + kRW && w1 > i0) || (b0 < i0 + kRW && b1 > i0);   // warp-uniform
+      if (!hit) {
+        if (lane == 0) *slot = 0.0;
+        continue;
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int ie = i + e;
+        if ((ie >= w0 && ie < w1) || (ie >= b0 && ie < b1)) acc += double(P[ie]) * g[e];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) *slot = acc;
+    }
   }
-  if (blockIdx.x == 0 && tid < 32) {
+  if (blockIdx.x == 0 && w == 1) {
     // loss terms of subdomain q: lane l sums chunks c0 + l, c0 + l + 32, ...; fixed shuffle tree
+    const int tid = lane;
     double l4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int c = c0 + tid; c < c1; c += 32) {
       const float4 v = __ldcg(reinterpret_cast<const float4*>(r.partial_loss) + c);
@@ -1021,21 +1048,30 @@ __global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
   // slope gradients: the block owning a^k combines K5a's
   // per-block partials in block order.  a^k = 0 leaves the identity
   // undefined: the gradient is set to NaN and flagged (never a silent 0).
-  if (r.mode != 2 && tid < r.n_hidden) {
-    const int oa = r.offA[tid];
+  // Warp k handles a^k: its lanes sum K5a's block partials of the blocks that
+  // overlap W^k / b^k (lane-strided, fixed order), then a fixed shuffle tree.
+  const int k = tid >> 5, lane = tid & 31;
+  if (r.mode != 2 && k < r.n_hidden) {
+    const int oa = r.offA[k];
     if (oa >= i0 && oa < i0 + kRB) {
+      const int bb0 = r.offW[k] / kRW, bb1 = (r.offB[k] + r.nB[k] - 1) / kRW + 1;
+      const double* sp = r.slope_part + size_t(q) * r.nb5a * kMaxHidden + k;
       double sum = 0.0;
-      for (int b = 0; b < int(gridDim.x); ++b) sum += r.slope_part[(size_t(q) * gridDim.x + b) * kMaxHidden + tid];
-      const double a = double(P[oa]);
-      float ga;
-      if (a == 0.0) {
-        ga = __int_as_float(0x7fc00000);
-        atomicOr(r.sflag + q, kFlagSlopeZero);
-      } else {
-        ga = float(sum / a);
-        if (!isfinite(ga)) atomicOr(r.sflag + q, kFlagSlopeGrad);
+      for (int b = bb0 + lane; b < bb1; b += 32) sum += sp[size_t(b) * kMaxHidden];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        const double a = double(P[oa]);
+        float ga;
+        if (a == 0.0) {
+          ga = __int_as_float(0x7fc00000);
+          atomicOr(r.sflag + q, kFlagSlopeZero);
+        } else {
+          ga = float(sum / a);
+          if (!isfinite(ga)) atomicOr(r.sflag + q, kFlagSlopeGrad);
+        }
+        G[oa] = ga;
       }
-      G[oa] = ga;
     }
   }
   __syncthreads();
@@ -1063,7 +1099,9 @@ __global__ void __launch_bounds__(kRB) k_slope_adam(const RArgs r) {
     if (prev == int(gridDim.x) - 1) {
       __threadfence();
       if (r.mode != 0) r.tstep[q] = t;
-      r.loss[size_t(q) * 8 + 5] = float(atomicOr(r.sflag + q, 0));
+      // publish this evaluation's status bits, then clear them for the next
+      // one (every K5a is followed by a K5b, so no memset node is needed)
+      if (r.mode != 2) r.loss[size_t(q) * 8 + 5] = float(atomicExch(r.sflag + q, 0));
       r.done[q] = 0;
       __threadfence();
     }
