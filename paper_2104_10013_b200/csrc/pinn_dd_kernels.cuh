@@ -80,17 +80,33 @@ __device__ __forceinline__ void load_weights(const float* __restrict__ G, float 
   const int tid = threadIdx.x;
   for (int e = tid; e < 3 * N; e += T) sm[C::oW1 + e] = G[LY::offW(1) + e];   // W^1 [N][2], b^1 (offB(1) = 2N)
   static_assert(LY::offB(1) == 2 * N && C::oB1 == 2 * N, "W^1/b^1 contiguous");
-  // hidden W^k rows: float4 copies; row j of layer k lands at j*WS + (j/kJT)*4
+  // hidden W^k rows: float4 copies; row j of layer k lands at j*WS + (j/kJT)*4.
+  // Every load of a layer is issued before its stores (one L2 round trip per
+  // layer, not one per float4: with C5's one-tile chunks of ten regions the
+  // weights are reloaded for most tiles, and the serial copy loop was 5 % of K1)
   constexpr int Q = N / 4;   // float4 per row
+  constexpr int IT = (N * Q + T - 1) / T;
 #pragma unroll 1
   for (int k = 2; k <= NH; ++k) {
     const float4* W = reinterpret_cast<const float4*>(G + LY::offW(k));
     float* dst = sm + C::oWh + (k - 2) * C::WROWS;
-    for (int e = tid; e < N * Q; e += T) {
-      const int j = e / Q, q = e - (e / Q) * Q;
-      *reinterpret_cast<float4*>(dst + j * C::WS + (j / kJT) * 4 + 4 * q) = W[e];
+    float4 v[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      if (e < N * Q) v[it] = __ldcg(W + e);
     }
-    for (int e = tid; e < N; e += T) sm[C::oBh + (k - 2) * N + e] = G[LY::offB(k) + e];
+    const float bk = tid < N ? G[LY::offB(k) + tid] : 0.0f;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int e = tid + it * T;
+      if (e < N * Q) {
+        const int j = e / Q, q = e - (e / Q) * Q;
+        *reinterpret_cast<float4*>(dst + j * C::WS + (j / kJT) * 4 + 4 * q) = v[it];
+      }
+    }
+    static_assert(N <= T, "one bias per thread");
+    if (tid < N) sm[C::oBh + (k - 2) * N + tid] = bk;
   }
   for (int e = tid; e < DO * N; e += T) {
     const int o = e / N, i = e - (e / N) * N;

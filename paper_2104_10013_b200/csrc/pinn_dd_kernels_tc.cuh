@@ -335,12 +335,25 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       // weights of subdomain ch.sub: W^k | b^k as tf32 operands, the rest FP32
       cta_sync();
       const float* G = a.params + size_t(ch.sub) * a.pstride;
+      // batches of 8 loads in flight per thread (one-tile chunks reload often)
       for (int k = 2; k <= NH; ++k) {
         float* dst = sW + (k - 2) * WOPER;
-        for (int e = tid; e < N * CP; e += T) {
-          const int j = e / CP, i = e % CP;
-          const float v = i < N ? G[LY::offW(k) + j * N + i] : (i == N ? G[LY::offB(k) + j] : 0.0f);
-          dst[sw32(j, i)] = to_tf32(v);
+#pragma unroll 1
+        for (int e0 = tid; e0 < N * CP; e0 += 8 * T) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * T;
+            const int j = e / CP, i = e % CP;
+            v[u] = e >= N * CP ? 0.0f
+                               : (i < N ? __ldcg(G + LY::offW(k) + j * N + i)
+                                        : (i == N ? __ldcg(G + LY::offB(k) + j) : 0.0f));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * T;
+            if (e < N * CP) dst[sw32(e / CP, e % CP)] = to_tf32(v[u]);
+          }
         }
       }
       float* s1 = sm + C::oW1;
