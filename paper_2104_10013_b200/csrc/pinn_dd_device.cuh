@@ -545,6 +545,14 @@ struct KArgs {
   int n_chunks2;
   const int32_t* order;     // [n_chunks] processing order (nullptr = identity)
   int32_t* sched;           // chunk counter, CTAs done (zero between launches); MODE 2: [4] payload chunks done
+  // MODE 2 sticky schedule (nullptr: one global queue in `order`): per-
+  // subdomain chunk queues, so that a CTA keeps its subdomain's weights in
+  // shared memory until that subdomain runs out of chunks
+  const int32_t* sub_list;      // chunk indices, subdomain-major
+  const int32_t* sub_list_off;  // [n_sub + 1]
+  int32_t* sub_ctr;             // [n_sub] claims (zero between launches)
+  const int32_t* sub_tiles;     // [n_sub + 1] cumulative tiles (first claim of each CTA)
+  int n_sub;
   int n_chunks;
   int64_t n_points;
   int pstride;              // floats per subdomain in params / partial

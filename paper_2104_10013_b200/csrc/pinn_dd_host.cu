@@ -273,6 +273,8 @@ struct pinn_dd {
   int32_t *pinfo = nullptr, *ptwin = nullptr, *sub_chunk = nullptr, *tstep = nullptr, *done = nullptr;
   double* slope_part = nullptr;
   int32_t *sflag = nullptr, *packmap = nullptr, *sub_act = nullptr, *order1 = nullptr, *sched = nullptr;
+  int32_t *sub_list = nullptr, *sub_list_off = nullptr, *sub_ctr = nullptr, *sub_tiles = nullptr;
+  int sub_list_tiles = 0;   // K1 tiles of all chunks (sticky-schedule heuristic)
   float2* segn = nullptr;
   float4 *sub_w = nullptr, *sub_adam = nullptr;
   Chunk *chunks1 = nullptr, *chunks2 = nullptr;
@@ -375,7 +377,7 @@ struct Carve {
 
 struct Layout {
   size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ord1,
-      sched, ch2, subch,
+      sched, ch2, subch, slist, sloff, sctr, stiles,
       tstep, done, sflag, loss, packmap, slopep, sendbuf, psend, dgeo, dpoly, dgeoloc, xflags, xstep, gstash,
       total;
 };
@@ -560,6 +562,11 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->dgeoloc = c.take<int32_t>(size_t(ngeo) + 1);
   L->xflags = c.take<unsigned long long>(kMaxPeers);
   L->xstep = c.take<int32_t>(1);
+  // fused step's per-subdomain chunk queues (sticky schedule)
+  L->slist = c.take<int32_t>(size_t(n1));
+  L->sloff = c.take<int32_t>(ns + 1);
+  L->sctr = c.take<int32_t>(ns);
+  L->stiles = c.take<int32_t>(ns + 1);
   L->gstash = (d->flags & PINN_DD_FLAG_GLOBAL_STASH)
                   ? c.take<float>(size_t(grid1) * d->n_hidden * kA * ops->threads)
                   : c.off;
@@ -601,6 +608,11 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.chunks2 = nullptr;
   a.n_chunks2 = 0;
   a.order = payload_tiles ? nullptr : h->order1;   // launch_k1 selects the part
+  a.sub_list = nullptr;                            // launch_fused: sticky queues
+  a.sub_list_off = nullptr;
+  a.sub_ctr = nullptr;
+  a.sub_tiles = nullptr;
+  a.n_sub = d.n_sub;
   a.sched = h->sched + (payload_tiles ? 2 : 0);
   a.n_chunks = payload_tiles ? h->n_chunks2 : h->n_chunks1;
   a.n_points = d.n_points;
@@ -736,6 +748,18 @@ pinn_dd_status launch_fused(pinn_dd* h) {
   // is left (C5's one-tile chunks interleaved them: 5 % of K1's samples were
   // the payload wait)
   a.order = h->order1 + h->n_chunks1;
+  // sticky per-subdomain queues (development A/B knob PINN_DD_NO_STICKY=1)
+  // Only where a CTA runs many small chunks (C5's one-tile chunks: K1 0.470
+  // -> 0.462 ms, TF32 0.358 -> 0.272 ms): with 4-tile chunks (C2: 8 per CTA)
+  // the per-subdomain queues lose the global largest-first tail balance (C2
+  // K1 1.345 -> 1.450 ms).
+  static const bool no_sticky = std::getenv("PINN_DD_NO_STICKY") != nullptr;
+  if (!no_sticky && h->n_chunks1 >= 6 * h->grid1 && h->sub_list_tiles <= 2 * h->n_chunks1) {
+    a.sub_list = h->sub_list;
+    a.sub_list_off = h->sub_list_off;
+    a.sub_ctr = h->sub_ctr;
+    a.sub_tiles = h->sub_tiles;
+  }
   if (h->peers_connected) a.px = h->px;
   h->ops->kf(a, std::min(h->grid1, a.n_chunks + a.n_chunks2), h->ops->smem, h->stream);
   ++h->launches;
@@ -969,6 +993,10 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->dgeo_local = reinterpret_cast<int32_t*>(base + L.dgeoloc);
   h->xflags = reinterpret_cast<unsigned long long*>(base + L.xflags);
   h->xstep = reinterpret_cast<int*>(base + L.xstep);
+  h->sub_list = reinterpret_cast<int32_t*>(base + L.slist);
+  h->sub_list_off = reinterpret_cast<int32_t*>(base + L.sloff);
+  h->sub_ctr = reinterpret_cast<int32_t*>(base + L.sctr);
+  h->sub_tiles = reinterpret_cast<int32_t*>(base + L.stiles);
 
   // ---- per-point classification and 1/N (Eq. 3/5/6; per-edge mean, Z2)
   const int64_t np = d->n_points;
@@ -1084,6 +1112,23 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   std::stable_sort(ord1.begin() + c1.size(), ord1.begin() + c1.size() + n_int, big_first);
   std::stable_sort(ord1.begin() + c1.size() + n_int, ord1.end(), big_first);
   h->n_int = n_int;
+  // per-subdomain queues of the fused step: residual + training chunks (big
+  // first), then interface chunks; cumulative tiles place the CTAs' first claims
+  std::vector<int32_t> slist, sloff(ns + 1, 0), stiles(ns + 1, 0);
+  for (int q = 0; q < ns; ++q) {
+    sloff[q] = int32_t(slist.size());
+    std::vector<int32_t> in, itf;
+    for (int32_t i = subch[q]; i < subch[q + 1]; ++i) (c1[i].pad ? itf : in).push_back(i);
+    std::stable_sort(in.begin(), in.end(), big_first);
+    std::stable_sort(itf.begin(), itf.end(), big_first);
+    slist.insert(slist.end(), in.begin(), in.end());
+    slist.insert(slist.end(), itf.begin(), itf.end());
+    int tiles = 0;
+    for (int32_t i = subch[q]; i < subch[q + 1]; ++i) tiles += (c1[i].count + P - 1) / P;
+    stiles[q + 1] = stiles[q] + tiles;
+  }
+  sloff[ns] = int32_t(slist.size());
+  h->sub_list_tiles = stiles[ns];
   std::vector<int32_t> pm;
   h->ops->packmap(pm);
   h->n_packed = int(pm.size());
@@ -1122,6 +1167,10 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   CKC(cudaMemcpyAsync(h->sub_adam, suba.data(), suba.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->chunks1, c1.data(), c1.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->order1, ord1.data(), ord1.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->sub_list, slist.data(), slist.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->sub_list_off, sloff.data(), sloff.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemcpyAsync(h->sub_tiles, stiles.data(), stiles.size() * 4, cudaMemcpyHostToDevice, st));
+  CKC(cudaMemsetAsync(h->sub_ctr, 0, ns * 4, st));
   CKC(cudaMemsetAsync(h->sched, 0, 8 * sizeof(int32_t), st));
   if (!c2.empty())
     CKC(cudaMemcpyAsync(h->chunks2, c2.data(), c2.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));

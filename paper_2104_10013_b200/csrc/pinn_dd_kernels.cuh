@@ -33,6 +33,26 @@ namespace pinn {
 #define PINN_UF_DW 8
 #endif
 constexpr int kUfFwd = PINN_UF_FWD, kUfDw = PINN_UF_DW;
+
+// Development build only (-DPINN_PHASE_PROF): thread 0 of every CTA charges
+// the clock cycles between phase marks to the phase that just ended; CTAs
+// 0..3 print their totals at exit (tools/phase_prof.sh).  Phases are CTA-
+// barrier delimited, so thread 0's split is the CTA's.
+#ifdef PINN_PHASE_PROF
+#define PROF_MARK(k)                                  \
+  do {                                                \
+    if (threadIdx.x == 0) {                           \
+      const long long t_ = clock64();                 \
+      prof_acc[prof_cur] += t_ - prof_t0;             \
+      prof_t0 = t_;                                   \
+      prof_cur = (k);                                 \
+    }                                                 \
+  } while (0)
+#else
+#define PROF_MARK(k) \
+  do {               \
+  } while (0)
+#endif
 constexpr int kUfBwd = PINN_UF_BWD;
 
 // CTA barrier preceded by an explicit warp reconvergence.
@@ -204,7 +224,6 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
   using C = KCfg<N, NH, DO, T>;
   constexpr int JB = C::JB, IB = C::IB, NJ = C::NJ, NI = C::NI, NBLK = C::NBLK, S = C::S;
   constexpr int PS = C::P / S;
-  constexpr int DBOFF = S * C::SSPL;
   const int tid = threadIdx.x;
   if (tid < NBLK * S) {
     const int r = tid % NBLK, s = tid / NBLK;
@@ -231,8 +250,10 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
           acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].x, zr[jj].y), make_float2(hr[ii].x, hr[ii].y), acc2[jj][ii]);
           acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].z, zr[jj].w), make_float2(hr[ii].z, hr[ii].w), acc2[jj][ii]);
         }
+      if constexpr (S == 1 && DWS) {
 #pragma unroll
-      for (int jj = 0; jj < JB; ++jj) db[jj] += zr[jj].x;
+        for (int jj = 0; jj < JB; ++jj) db[jj] += zr[jj].x;
+      }
     }
     float acc[JB][IB];
 #pragma unroll
@@ -255,14 +276,12 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
         if (ib == 0) accB[jb + NJ * jj] = curb[jj] + db[jj];
       }
     } else {
+      // db^k is summed once per row by db_sum (the NI threads of a row block
+      // used to repeat it: 5 FADDs per point, 10 % of the FMA-pipe cycles of dW)
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
         for (int ii = 0; ii < IB; ++ii) sDw[s * C::SSPL + (jb + NJ * jj) * C::SROW + ib + NI * ii] = acc[jj][ii];
-      if (ib == 0) {
-#pragma unroll
-        for (int jj = 0; jj < JB; ++jj) sDw[DBOFF + s * N + jb + NJ * jj] = db[jj];
-      }
     }
   }
 }
@@ -274,6 +293,32 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 // Global chunk partial (!DWS) with few entries per thread: its current values
 // are loaded right after gemm_dw (before gemm_bwd and the barrier), so the L2
 // round trip overlaps the input-adjoint GEMM instead of following the barrier.
+// db^k[j] = sum_p Zb^k[j][p].value for thread j < N (4 interleaved chains,
+// combined in fixed order).  Called after the input-adjoint GEMM and before
+// the barrier that precedes the next writes of the Zb buffer.
+template <int N, int NH, int DO, int T, bool DWS>
+__device__ __forceinline__ float db_sum(const float4* __restrict__ Zb) {
+  using C = KCfg<N, NH, DO, T>;
+  if constexpr (C::S == 1 && DWS) {
+    return 0.0f;   // gemm_dw accumulates db itself on this path
+  } else {
+    static_assert(C::P % 4 == 0, "four chains");
+    const int tid = threadIdx.x;
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    if (tid < N) {
+      const float4* z = Zb + C::row(tid);
+#pragma unroll 8
+      for (int p = 0; p < C::P; p += 4) {
+        a0 += z[p].x;
+        a1 += z[p + 1].x;
+        a2 += z[p + 2].x;
+        a3 += z[p + 3].x;
+      }
+    }
+    return (a0 + a1) + (a2 + a3);
+  }
+}
+
 template <int N, int NH, int DO, int T, bool DWS>
 struct DwPre {
   static constexpr int IT = (N * N + T - 1) / T;
@@ -297,10 +342,9 @@ __device__ __forceinline__ void gemm_dw_prefetch(const float* accW, const float*
 
 template <int N, int NH, int DO, int T, bool DWS>
 __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool first, const float* sDw,
-                                               const float* pre, float preb) {
+                                               const float* pre, float preb, float dbv) {
   using C = KCfg<N, NH, DO, T>;
   constexpr int S = C::S;
-  constexpr int DBOFF = S * C::SSPL;
   constexpr bool PRE = DwPre<N, NH, DO, T, DWS>::ON;
   if constexpr (!DWS || S > 1) {
     // thread e owns dW entries e, e + T, ... in natural [j][i] order: the
@@ -337,9 +381,7 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
       if (e < NE) accW[e] = (DWS || !first) ? cur[it] + v[it] : v[it];
     }
     if (tid < N) {
-      float x = 0.0f;
-#pragma unroll
-      for (int s = 0; s < S; ++s) x += sDw[DBOFF + s * N + tid];
+      const float x = dbv;   // db_sum
       if constexpr (PRE)
         accB[tid] = first ? x : preb + x;
       else
@@ -426,6 +468,55 @@ __device__ __forceinline__ void wait_payload(const KArgs& a, int n_pay, int step
   }
 }
 
+// Sticky schedule (MODE 2): thread 0 claims the next chunk of subdomain q,
+// else of the next subdomains in turn (q + 1, q + 2, ...); returns the chunk
+// index, or -1 when every queue is empty.  A CTA's first subdomain comes from
+// its position in the cumulative tile count, so the CTAs start spread over the
+// subdomains in proportion to their work.  Which CTA runs a chunk never
+// changes its result (every chunk owns its partial slot).
+__device__ __forceinline__ int sticky_first_sub(const KArgs& a) {
+  const long long tot = a.sub_tiles[a.n_sub];
+  const long long target = ((2LL * blockIdx.x + 1) * tot) / (2LL * gridDim.x);
+  int q = 0;
+  while (q + 1 < a.n_sub && a.sub_tiles[q + 1] <= target) ++q;
+  return q;
+}
+__device__ __forceinline__ int sticky_claim(const KArgs& a, int& q) {
+  for (int d = 0; d < a.n_sub; ++d) {
+    int qq = q + d;
+    if (qq >= a.n_sub) qq -= a.n_sub;
+    const int n = a.sub_list_off[qq + 1] - a.sub_list_off[qq];
+    if (*reinterpret_cast<volatile int*>(a.sub_ctr + qq) >= n) continue;
+    const int k = atomicAdd(a.sub_ctr + qq, 1);
+    if (k < n) {
+      q = qq;
+      return a.sub_list[a.sub_list_off[qq] + k];
+    }
+  }
+  return -1;
+}
+// next work item of a persistent CTA (thread 0): payload chunks [0, n_pay)
+// from the global counter first, then loss chunks n_pay + c -- chunk c
+// directly when sticky, else the position in `order`
+// (thread 0's state lives in shared memory, st[0] = current subdomain or -1
+// before the first claim, st[1] = 1 once the global payload queue is empty:
+// registers carried across the tile loop cost the 255-register TF32 kernel 9 %)
+__device__ __forceinline__ int next_item(const KArgs& a, int n_pay, volatile int* st) {
+  if (st[1] == 0) {
+    const int idx = atomicAdd(a.sched, 1);
+    if (a.sub_list == nullptr || idx < n_pay) return idx;
+    st[1] = 1;
+  }
+  int q = st[0] < 0 ? sticky_first_sub(a) : st[0];
+  const int c = sticky_claim(a, q);
+  st[0] = q;
+  return c < 0 ? a.n_chunks + n_pay : n_pay + c;
+}
+__device__ __forceinline__ void sticky_reset(const KArgs& a) {
+  if (a.sub_list)
+    for (int q = 0; q < a.n_sub; ++q) a.sub_ctr[q] = 0;
+}
+
 // epilogue of one point (K1): its loss terms (Eq. 3/5/6; lsum = MSE_u, MSE_F,
 // MSE_uavg, MSE_if partials) and the adjoint seeds Ub = dJ/dU (a8)
 template <int DO>
@@ -493,6 +584,25 @@ __device__ __forceinline__ void point_adjoint(const KArgs& a, int64_t gp, float 
   }
 }
 
+// Runs f(integral_constant<AS>) with the chunk's activation: the compiled one,
+// or -- per-subdomain (kActMixed) instances -- a branch on the runtime `act`
+// (uniform per chunk) around the small activation loop only, so the GEMM code
+// exists once per kernel instead of once per activation (C5's kernel was
+// three copies of everything: 0.36 no-instruction stalls per issue).
+template <int ACT, class F>
+__device__ __forceinline__ void with_act(int act, F&& f) {
+  if constexpr (ACT != kActMixed) {
+    f(std::integral_constant<int, ACT>{});
+  } else {
+    if (act == 0)
+      f(std::integral_constant<int, 0>{});
+    else if (act == 1)
+      f(std::integral_constant<int, 1>{});
+    else
+      f(std::integral_constant<int, 2>{});
+  }
+}
+
 template <int N, int NH, int DO, int ACT, int MODE, int T>
 __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   using C = KCfg<N, NH, DO, T>;
@@ -527,6 +637,11 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::TOTAL - 4);
   const float m1 = a.m1, m2 = a.m2;
 
+#ifdef PINN_PHASE_PROF
+  long long prof_acc[20] = {};
+  long long prof_t0 = clock64();
+  int prof_cur = 0;
+#endif
   Stash st;
   st.tid = tid;
   st.nthr = T;
@@ -566,15 +681,22 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   const int xstep = px ? *reinterpret_cast<volatile int*>(a.px.step) : 0;
   const int64_t roff = px ? int64_t(xstep & 1) * a.px.n_recv : 0;
   if (tid < kMaxPeers) xcount[tid] = 0;
+  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::TOTAL - 2);   // sticky state (next_item)
+  if (tid == 0) {
+    sst[0] = -1;
+    sst[1] = 0;
+  }
 #pragma unroll 1
   for (;;) {
-    if (tid == 0) s_next = atomicAdd(a.sched, 1);
+    PROF_MARK(0);
+    if (tid == 0) s_next = MODE == 2 ? next_item(a, n_pay, sst) : atomicAdd(a.sched, 1);
     cta_sync();
     const int idx = s_next;
     if (idx >= a.n_chunks + n_pay) break;
     const bool pay = MODE == 1 || (MODE == 2 && idx < n_pay);   // payload chunk (forward + payload epilogue)
     const int li = idx - n_pay;
-    const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (a.order ? a.order[li] : li);
+    const bool direct = MODE == 2 && a.sub_list != nullptr;     // sticky: li is the chunk index
+    const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (direct ? li : (a.order ? a.order[li] : li));
     const Chunk ch = (MODE == 2 && pay) ? a.chunks2[c] : a.chunks[c];
     if (MODE == 2 && !pay && ch.pad) {
       // interface loss chunk: acquire the completed payload rows (local, and the peers')
@@ -583,9 +705,11 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     }
     if (ch.sub != cur_sub) {
       cta_sync();
+      PROF_MARK(1);
       load_weights<N, NH, DO, T>(a.params + size_t(ch.sub) * a.pstride, a.slope_n, sm);
       cur_sub = ch.sub;
     }
+    PROF_MARK(0);
     const float4 lw = a.sub_w[ch.sub];
     const int act = ACT == kActMixed ? a.sub_act[ch.sub] : ACT;   // uniform per chunk
     float* Pc = a.partial + size_t(c) * a.pstride;
@@ -602,11 +726,10 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         if (tid < 4) a.partial_loss[size_t(c) * 4 + tid] = 0.0f;
       }
     }
-    // the chunk's tiles, compiled once per activation: the per-subdomain-activation
-    // instance dispatches here per chunk, so each hot loop holds one activation
-    // path only (three inlined paths overflowed the instruction cache)
-    auto chunk_body = [&](auto act_c, auto mode_c) {
-      constexpr int AS = decltype(act_c)::value;
+    // the chunk's tiles, compiled once per mode (payload / loss); a per-
+    // subdomain-activation instance branches on `act` around each activation
+    // loop only (with_act), never around the GEMMs
+    auto chunk_body = [&](auto mode_c) {
       constexpr int MS = decltype(mode_c)::value;   // 0 loss + gradient, 1 payload
       // coordinates of the next tile are loaded into registers while the
       // current tile computes (thread p < P owns point p of a tile)
@@ -622,6 +745,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         const int64_t p0 = int64_t(ch.start) + int64_t(t) * C::P;
         const int np = min(C::P, ch.count - t * C::P);
         const bool first = (t == 0);
+        PROF_MARK(MS == 1 ? 10 : 2);
         cta_sync();
         if (tid < C::P) {
           sX[tid] = cx;
@@ -634,6 +758,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         }
         cta_sync();
 
+        PROF_MARK(MS == 1 ? 10 : 3);
         // ------------------------------------------------------------ forward
         float4 z[kJT];   // this thread's neurons' jets (value, d1, d2, Delta_S)
         {
@@ -646,26 +771,36 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             z[jj] = make_float4(fmaf(w0, x, fmaf(w1, y, sB1[j])), w0, w1, 0.0f);
           }
           const float s = sSl[0];
+          with_act<ACT>(act, [&](auto act_c) {
+            constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
-          if constexpr (MS == 0) st.store(0, reinterpret_cast<const float*>(z));
+            for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
+            if constexpr (MS == 0) st.store(0, reinterpret_cast<const float*>(z));
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) buf0[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
+            for (int jj = 0; jj < kJT; ++jj) buf0[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
+          });
         }
         cta_sync();
 #pragma unroll 1
         for (int k = 2; k <= NH; ++k) {
           const float4* Hin = (k & 1) ? buf1 : buf0;
           float4* Hout = (k & 1) ? buf0 : buf1;
+          PROF_MARK(MS == 1 ? 10 : 12);
           gemm_fwd<N, NH, DO, T, kUfFwd>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
+          PROF_MARK(MS == 1 ? 10 : 13);
           const float s = sSl[k - 1];
+          with_act<ACT>(act, [&](auto act_c) {
+            constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
-          if constexpr (MS == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
+            for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
+            if constexpr (MS == 0) st.store(k - 1, reinterpret_cast<const float*>(z));
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) Hout[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
+            for (int jj = 0; jj < kJT; ++jj) Hout[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s, m1, m2, act);
+          });
+          PROF_MARK(MS == 1 ? 10 : 14);
           cta_sync();
         }
+        PROF_MARK(MS == 1 ? 10 : 4);
         const float4* HL = (NH & 1) ? buf0 : buf1;   // H^{NH}
         // output layer: 4 lanes per (point, output), each over every 4th input,
         // combined by a fixed xor-shuffle tree (short dependent chains)
@@ -689,6 +824,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         }
         cta_sync();
 
+        PROF_MARK(MS == 1 ? 11 : 5);
         // ----------------------------------------------------------- epilogue
         if constexpr (MS == 1) {
           // payload: u(x_I) and f.n (cPINN) or F (XPINN) (Algorithm 1)
@@ -713,6 +849,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           }
           cta_sync();
 
+          PROF_MARK(6);
           // ------------------------------------------------------------ reverse
           // output layer: dW^L, db^L
           for (int t4 = tid; t4 < 4 * DO * N; t4 += T) {   // warp-uniform trip count
@@ -757,18 +894,25 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           {
             st.load(NH - 1, reinterpret_cast<float*>(z));
             const float s = sSl[NH - 1];
+            with_act<ACT>(act, [&](auto act_c) {
+              constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+              for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+            });
             if (NH >= 2) {
               st.load(NH - 2, reinterpret_cast<float*>(z));
               const float s2 = sSl[NH - 2];
+              with_act<ACT>(act, [&](auto act_c) {
+                constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-              for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+                for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+              });
             }
           }
           float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
           float4* bufH = buf1;   // activation of the layer below
           cta_sync();
+          PROF_MARK(7);
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) {
             bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
@@ -778,24 +922,36 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
 #pragma unroll 1
           for (int k = NH; k >= 2; --k) {
             // dW^k, db^k
+            PROF_MARK(15);
             gemm_dw<N, NH, DO, T, DSM, kUfDw>(bufZ, bufH, A + LY::offW(k), A + LY::offB(k), first, sDw);   // partials
             float pre[DwPre<N, NH, DO, T, DSM>::IT], preb = 0.0f;
             gemm_dw_prefetch<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, pre, preb);
             // adjoint of H^{k-1}, then of Z^{k-1}
+            PROF_MARK(16);
             gemm_bwd<N, NH, DO, T>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
+            PROF_MARK(17);
             st.load(k - 2, reinterpret_cast<float*>(z));
             const float s = sSl[k - 2];
+            with_act<ACT>(act, [&](auto act_c) {
+              constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-            for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+              for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+            });
             const bool more = (k - 1 >= 2);
             if (more) {
               st.load(k - 3, reinterpret_cast<float*>(z));
               const float s2 = sSl[k - 3];
+              with_act<ACT>(act, [&](auto act_c) {
+                constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-              for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+                for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+              });
             }
+            const float dbv = db_sum<N, NH, DO, T, DSM>(bufZ);
+            PROF_MARK(18);
             cta_sync();
-            gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw, pre, preb);
+            PROF_MARK(19);
+            gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw, pre, preb, dbv);
 #pragma unroll
             for (int jj = 0; jj < kJT; ++jj) {
               bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
@@ -803,6 +959,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             }
             cta_sync();
           }
+          PROF_MARK(8);
           // layer 1: dW^1[j] = sum_p zb_v x_p + zb_{d_i}; db^1 = sum_p zb_v
           for (int t4 = tid; t4 < 4 * N; t4 += T) {
             const int qq = t4 & 3, j = t4 >> 2;
@@ -844,6 +1001,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           }
         }
       }
+      PROF_MARK(9);
       if constexpr (MS == 0) {
         // loss partials of the chunk: fixed-order block reduction once per chunk
         if (ntiles > 0) {
@@ -855,25 +1013,13 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
         }
       }
     };
-    auto by_mode = [&](auto act_c) {
-      if constexpr (MODE == 2) {
-        if (pay)
-          chunk_body(act_c, std::integral_constant<int, 1>{});
-        else
-          chunk_body(act_c, std::integral_constant<int, 0>{});
-      } else {
-        chunk_body(act_c, std::integral_constant<int, MODE>{});
-      }
-    };
-    if constexpr (ACT == kActMixed) {
-      if (act == 0)
-        by_mode(std::integral_constant<int, 0>{});
-      else if (act == 1)
-        by_mode(std::integral_constant<int, 1>{});
+    if constexpr (MODE == 2) {
+      if (pay)
+        chunk_body(std::integral_constant<int, 1>{});
       else
-        by_mode(std::integral_constant<int, 2>{});
+        chunk_body(std::integral_constant<int, 0>{});
     } else {
-      by_mode(std::integral_constant<int, ACT>{});
+      chunk_body(std::integral_constant<int, MODE>{});
     }
     if (MODE == 2 && pay) {
       // publish this payload chunk (release: all its rows are written)
@@ -891,6 +1037,15 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     }
     cta_sync();   // every thread has read s_next before it is overwritten
   }
+#ifdef PINN_PHASE_PROF
+  PROF_MARK(0);
+  if (tid == 0 && blockIdx.x < 4)
+    printf("PHASE N=%d NH=%d MODE=%d cta=%d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld "
+           "%lld %lld %lld %lld %lld\n", N, NH, MODE, int(blockIdx.x), prof_acc[0], prof_acc[1], prof_acc[2],
+           prof_acc[3], prof_acc[4], prof_acc[5], prof_acc[6], prof_acc[7], prof_acc[8], prof_acc[9], prof_acc[10],
+           prof_acc[11], prof_acc[12], prof_acc[13], prof_acc[14], prof_acc[15], prof_acc[16], prof_acc[17],
+           prof_acc[18], prof_acc[19]);
+#endif
   // the last CTA to leave re-arms the counter for the next launch
   if (tid == 0) {
     __threadfence();
@@ -898,6 +1053,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
       a.sched[0] = 0;
       a.sched[1] = 0;
       if (MODE == 2) a.sched[4] = 0;
+      if (MODE == 2) sticky_reset(a);
       if (px) *a.px.step = xstep + 1;
       __threadfence();
     }

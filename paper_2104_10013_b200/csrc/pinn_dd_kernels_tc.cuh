@@ -229,7 +229,7 @@ struct TcCfg {
   static constexpr int oX = al4(oSl + NH);                   // [2][P]
   static constexpr int oU = oX + 2 * P;                      // [P][DO] float4
   static constexpr int oMisc = oU + 4 * P * DO;              // loss scratch [8][4], mbarrier, tmem slot, s_next
-  static constexpr int TOTAL = oMisc + 32 + 16;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts
+  static constexpr int TOTAL = oMisc + 32 + 16;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts, sticky state
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget of the tensor-core kernel");
   static_assert((oH * 4) % 1024 == 0 && (oZ * 4) % 1024 == 0 && (WOPER * 4) % 1024 == 0, "operand alignment");
@@ -317,15 +317,26 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   const int xstep = px ? *reinterpret_cast<volatile int*>(a.px.step) : 0;
   const int64_t roff = px ? int64_t(xstep & 1) * a.px.n_recv : 0;
   if (tid < kMaxPeers) xcount[tid] = 0;
+  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::oMisc + 46);   // sticky state (next_item)
+  if (tid == 0) {
+    sst[0] = -1;
+    sst[1] = 0;
+  }
 #pragma unroll 1
   for (;;) {
-    if (tid == 0) *s_next = atomicAdd(a.sched, 1);
+    // The sticky schedule is compiled into the per-region-activation instance
+    // only (C5: K1 0.324 -> 0.265 ms); in the 255-register 5x80 instance its
+    // mere presence costs 9 % (C4 TF32 K1 5.61 -> 6.08 ms) and C4's big
+    // chunks never use it.
+    constexpr bool kSticky = MODE == 2 && ACT == kActMixed;
+    if (tid == 0) *s_next = kSticky ? next_item(a, n_pay, sst) : atomicAdd(a.sched, 1);
     cta_sync();
     const int idx = *s_next;
     if (idx >= a.n_chunks + n_pay) break;
     const bool pay = MODE == 1 || (MODE == 2 && idx < n_pay);
     const int li = idx - n_pay;
-    const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (a.order ? a.order[li] : li);
+    const bool direct = kSticky && a.sub_list != nullptr;   // sticky: li is the chunk index
+    const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (direct ? li : (a.order ? a.order[li] : li));
     const Chunk ch = (MODE == 2 && pay) ? a.chunks2[c] : a.chunks[c];
     if (MODE == 2 && !pay && ch.pad) {
       wait_payload(a, n_pay, xstep);   // local payload chunks and the peers' rows
@@ -335,25 +346,12 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       // weights of subdomain ch.sub: W^k | b^k as tf32 operands, the rest FP32
       cta_sync();
       const float* G = a.params + size_t(ch.sub) * a.pstride;
-      // batches of 8 loads in flight per thread (one-tile chunks reload often)
       for (int k = 2; k <= NH; ++k) {
         float* dst = sW + (k - 2) * WOPER;
-#pragma unroll 1
-        for (int e0 = tid; e0 < N * CP; e0 += 8 * T) {
-          float v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + u * T;
-            const int j = e / CP, i = e % CP;
-            v[u] = e >= N * CP ? 0.0f
-                               : (i < N ? __ldcg(G + LY::offW(k) + j * N + i)
-                                        : (i == N ? __ldcg(G + LY::offB(k) + j) : 0.0f));
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + u * T;
-            if (e < N * CP) dst[sw32(e / CP, e % CP)] = to_tf32(v[u]);
-          }
+        for (int e = tid; e < N * CP; e += T) {
+          const int j = e / CP, i = e % CP;
+          const float v = i < N ? G[LY::offW(k) + j * N + i] : (i == N ? G[LY::offB(k) + j] : 0.0f);
+          dst[sw32(j, i)] = to_tf32(v);
         }
       }
       float* s1 = sm + C::oW1;
@@ -665,6 +663,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       a.sched[0] = 0;
       a.sched[1] = 0;
       if (MODE == 2) a.sched[4] = 0;
+      if (MODE == 2) sticky_reset(a);
       if (px) *a.px.step = xstep + 1;
       __threadfence();
     }

@@ -1,0 +1,27 @@
+#!/bin/bash
+# per-phase cycle split of K1 for each workload (development tool; run on the GPU box)
+# usage: tools/phase_prof.sh WORKLOAD...   (needs paper_2104_10013_b200/libpinn_dd_prof.so)
+set -u
+L=paper_2104_10013_b200
+cp $L/libpinn_dd.so /tmp/libpinn_dd_real.so
+cp $L/libpinn_dd_prof.so $L/libpinn_dd.so
+for w in "$@"; do
+  python tools/phase_prof.py $w 2>&1 | sed -n '/---MARK---/,$p' | python -c "
+import sys
+names = ['claim/setup', 'weights', 'coords', 'layer-1 fwd', 'output fwd', 'epilogue', 'output bwd', 'bwd prologue',
+         'layer-1 bwd', 'chunk end', 'payload fwd', 'payload epi', 'fwd: gemm', 'fwd: act+st', 'fwd: bar',
+         'bwd: dW', 'bwd: gemm_bwd', 'bwd: act', 'bwd: bar', 'bwd: red+st+bar']
+tot = [0] * 20
+hdr = ''
+for l in sys.stdin:
+    if l.startswith('---'): hdr = l.strip(); continue
+    if l.startswith('PHASE'):
+        v = [int(x) for x in l.split(':')[1].split()]
+        tot = [a + b for a, b in zip(tot, v)]
+s = sum(tot) or 1
+print(hdr, 'total Mcyc (4 CTAs) %.2f' % (s / 1e6))
+for n, t in zip(names, tot):
+    print('  %-12s %6.1f %%' % (n, 100 * t / s))
+"
+done
+cp /tmp/libpinn_dd_real.so $L/libpinn_dd.so
