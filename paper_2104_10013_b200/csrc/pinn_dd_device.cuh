@@ -124,7 +124,7 @@ struct KCfg {
   // accumulator in global memory, to coalesce the per-tile read-modify-write
   static constexpr int SCR = (S > 1 || !DW_SMEM) ? SCR1 : 0;
   static constexpr int oAcc = al4(oDw + SCR);              // per-chunk gradient accumulator
-  static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 12);  // + peer row counts [8], tmem slot, s_next
+  static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 16);  // + peer row counts [8], tmem slot, s_next, sticky state [4]
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= SMEM_CAP, "shared memory budget");
   static_assert(NBLK * S <= T, "dW blocks per CTA");

@@ -481,7 +481,7 @@ __device__ __forceinline__ int sticky_first_sub(const KArgs& a) {
   while (q + 1 < a.n_sub && a.sub_tiles[q + 1] <= target) ++q;
   return q;
 }
-__device__ __forceinline__ int sticky_claim(const KArgs& a, int& q) {
+__device__ __forceinline__ int sticky_claim(const KArgs& a, int& q, int& kq) {
   for (int d = 0; d < a.n_sub; ++d) {
     int qq = q + d;
     if (qq >= a.n_sub) qq -= a.n_sub;
@@ -490,6 +490,7 @@ __device__ __forceinline__ int sticky_claim(const KArgs& a, int& q) {
     const int k = atomicAdd(a.sub_ctr + qq, 1);
     if (k < n) {
       q = qq;
+      kq = k;
       return a.sub_list[a.sub_list_off[qq] + k];
     }
   }
@@ -498,19 +499,50 @@ __device__ __forceinline__ int sticky_claim(const KArgs& a, int& q) {
 // next work item of a persistent CTA (thread 0): payload chunks [0, n_pay)
 // from the global counter first, then loss chunks n_pay + c -- chunk c
 // directly when sticky, else the position in `order`
-// (thread 0's state lives in shared memory, st[0] = current subdomain or -1
-// before the first claim, st[1] = 1 once the global payload queue is empty:
-// registers carried across the tile loop cost the 255-register TF32 kernel 9 %)
+// (thread 0's state lives in shared memory: st[0] = current subdomain or -1
+// before the first claim, st[1] = 1 once the global payload queue is empty,
+// st[2] = a chunk claimed ahead (-1: none), st[3] = the current chunk's place
+// in its queue)
 __device__ __forceinline__ int next_item(const KArgs& a, int n_pay, volatile int* st) {
+  if (st[2] >= 0) {
+    const int c = st[2];
+    st[2] = -1;
+    return n_pay + c;
+  }
   if (st[1] == 0) {
     const int idx = atomicAdd(a.sched, 1);
     if (a.sub_list == nullptr || idx < n_pay) return idx;
     st[1] = 1;
   }
-  int q = st[0] < 0 ? sticky_first_sub(a) : st[0];
-  const int c = sticky_claim(a, q);
+  int q = st[0] < 0 ? sticky_first_sub(a) : st[0], kq = 0;
+  const int c = sticky_claim(a, q, kq);
   st[0] = q;
+  st[3] = kq;
   return c < 0 ? a.n_chunks + n_pay : n_pay + c;
+}
+// Claim-ahead (thread 0, sticky phase; the TF32 kernel only -- the FP32 one
+// measured 2 % slower with it): at the start of a chunk, claim the next chunk
+// of the same queue so the atomic's round trip overlaps the tiles (C5 TF32 K1
+// 0.265 -> 0.258 ms); only while >= kAheadMin chunks remain behind it, so the
+// schedule's tail is claimed one at a time as before.
+// Returns the claimed place in the queue (or -1); sticky_ahead_finish turns it
+// into st[2] after the chunk.
+constexpr int kAheadMin = 16;
+__device__ __forceinline__ int sticky_ahead_issue(const KArgs& a, volatile int* st) {
+  if (a.sub_list == nullptr || st[1] == 0 || st[0] < 0) return -1;
+  const int q = st[0];
+  const int n = a.sub_list_off[q + 1] - a.sub_list_off[q];
+  if (st[3] + kAheadMin >= n) return -1;
+  return atomicAdd(a.sub_ctr + q, 1);
+}
+__device__ __forceinline__ void sticky_ahead_finish(const KArgs& a, volatile int* st, int k) {
+  if (k < 0) return;
+  const int q = st[0];
+  const int n = a.sub_list_off[q + 1] - a.sub_list_off[q];
+  if (k < n) {
+    st[2] = a.sub_list[a.sub_list_off[q] + k];
+    st[3] = k;
+  }
 }
 __device__ __forceinline__ void sticky_reset(const KArgs& a) {
   if (a.sub_list)
@@ -634,7 +666,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   float* sDw = sm + C::oDw;
   float* sAcc = sm + C::oAcc;
   constexpr bool DSM = C::DW_SMEM;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::TOTAL - 4);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + C::TOTAL - 8);
   const float m1 = a.m1, m2 = a.m2;
 
 #ifdef PINN_PHASE_PROF
@@ -671,8 +703,8 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   // payload chunks (K2's work), then the loss chunks; an interface loss chunk
   // waits until every payload chunk is done (all CTAs are resident and payload
   // chunks are handed out first, so the wait always ends).
-  int& s_next = *reinterpret_cast<int*>(sm + C::TOTAL - 3);   // next chunk index (dynamic smem, after tslot)
-  int* xcount = reinterpret_cast<int*>(sm + C::TOTAL - 12);    // [kMaxPeers] peer rows of a payload chunk
+  int& s_next = *reinterpret_cast<int*>(sm + C::TOTAL - 7);   // next chunk index (dynamic smem, after tslot)
+  int* xcount = reinterpret_cast<int*>(sm + C::TOTAL - 16);    // [kMaxPeers] peer rows of a payload chunk
   int cur_sub = -1;
   const int n_pay = MODE == 2 ? a.n_chunks2 : 0;
   // peer-store exchange of the fused step: this launch's step index (receive
@@ -681,10 +713,12 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   const int xstep = px ? *reinterpret_cast<volatile int*>(a.px.step) : 0;
   const int64_t roff = px ? int64_t(xstep & 1) * a.px.n_recv : 0;
   if (tid < kMaxPeers) xcount[tid] = 0;
-  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::TOTAL - 2);   // sticky state (next_item)
+  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::TOTAL - 6);   // sticky state [4] (next_item)
   if (tid == 0) {
     sst[0] = -1;
     sst[1] = 0;
+    sst[2] = -1;
+    sst[3] = 0;
   }
 #pragma unroll 1
   for (;;) {

@@ -229,7 +229,7 @@ struct TcCfg {
   static constexpr int oX = al4(oSl + NH);                   // [2][P]
   static constexpr int oU = oX + 2 * P;                      // [P][DO] float4
   static constexpr int oMisc = oU + 4 * P * DO;              // loss scratch [8][4], mbarrier, tmem slot, s_next
-  static constexpr int TOTAL = oMisc + 32 + 16;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts, sticky state
+  static constexpr int TOTAL = oMisc + 32 + 20;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts, sticky state
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget of the tensor-core kernel");
   static_assert((oH * 4) % 1024 == 0 && (oZ * 4) % 1024 == 0 && (WOPER * 4) % 1024 == 0, "operand alignment");
@@ -321,6 +321,8 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   if (tid == 0) {
     sst[0] = -1;
     sst[1] = 0;
+    sst[2] = -1;
+    sst[3] = 0;
   }
 #pragma unroll 1
   for (;;) {
@@ -361,6 +363,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       for (int e = tid; e < NH; e += T) sm[C::oSl + e] = a.slope_n * G[LY::offA(e + 1)];
       cur_sub = ch.sub;
     }
+    const int ahead = (kSticky && !pay && tid == 0) ? sticky_ahead_issue(a, sst) : -1;
     const float4 lw = a.sub_w[ch.sub];
     const int act = ACT == kActMixed ? a.sub_act[ch.sub] : ACT;
     float* Pc = a.partial + size_t(c) * a.pstride;
@@ -655,6 +658,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
         atomicAdd(a.sched + 4, 1);
       }
     }
+    if (kSticky && tid == 0) sticky_ahead_finish(a, sst, ahead);
     cta_sync();
   }
   if (tid == 0) {
