@@ -548,8 +548,7 @@ struct KArgs {
   // MODE 2 sticky schedule (nullptr: one global queue in `order`): per-
   // subdomain chunk queues, so that a CTA keeps its subdomain's weights in
   // shared memory until that subdomain runs out of chunks
-  const int32_t* sub_list;      // chunk indices, subdomain-major
-  const int32_t* sub_list_off;  // [n_sub + 1]
+  const int32_t* sub_chunk_off; // [n_sub + 1] each subdomain's chunks (contiguous, in claim order)
   int32_t* sub_ctr;             // [n_sub] claims (zero between launches)
   const int32_t* sub_tiles;     // [n_sub + 1] cumulative tiles (first claim of each CTA)
   int n_sub;

@@ -273,8 +273,9 @@ struct pinn_dd {
   int32_t *pinfo = nullptr, *ptwin = nullptr, *sub_chunk = nullptr, *tstep = nullptr, *done = nullptr;
   double* slope_part = nullptr;
   int32_t *sflag = nullptr, *packmap = nullptr, *sub_act = nullptr, *order1 = nullptr, *sched = nullptr;
-  int32_t *sub_list = nullptr, *sub_list_off = nullptr, *sub_ctr = nullptr, *sub_tiles = nullptr;
-  int sub_list_tiles = 0;   // K1 tiles of all chunks (sticky-schedule heuristic)
+  int32_t *sub_ctr = nullptr, *sub_tiles = nullptr;
+  int sub_list_tiles = 0;      // K1 tiles of all chunks (sticky-schedule heuristic)
+  bool sticky_order = false;   // each subdomain's chunks are already in claim order
   float2* segn = nullptr;
   float4 *sub_w = nullptr, *sub_adam = nullptr;
   Chunk *chunks1 = nullptr, *chunks2 = nullptr;
@@ -377,7 +378,7 @@ struct Carve {
 
 struct Layout {
   size_t params, m, v, grad, scratch, partial, ploss, payload, pinfo, pinv, ptwin, segn, subw, suba, subact, ch1, ord1,
-      sched, ch2, subch, slist, sloff, sctr, stiles,
+      sched, ch2, subch, sctr, stiles,
       tstep, done, sflag, loss, packmap, slopep, sendbuf, psend, dgeo, dpoly, dgeoloc, xflags, xstep, gstash,
       total;
 };
@@ -563,8 +564,6 @@ pinn_dd_status plan(const pinn_dd_desc* d, pinn_dd* h, Layout* L, int nsm) {
   L->xflags = c.take<unsigned long long>(kMaxPeers);
   L->xstep = c.take<int32_t>(1);
   // fused step's per-subdomain chunk queues (sticky schedule)
-  L->slist = c.take<int32_t>(size_t(n1));
-  L->sloff = c.take<int32_t>(ns + 1);
   L->sctr = c.take<int32_t>(ns);
   L->stiles = c.take<int32_t>(ns + 1);
   L->gstash = (d->flags & PINN_DD_FLAG_GLOBAL_STASH)
@@ -608,8 +607,7 @@ KArgs make_kargs(pinn_dd* h, bool payload_tiles) {
   a.chunks2 = nullptr;
   a.n_chunks2 = 0;
   a.order = payload_tiles ? nullptr : h->order1;   // launch_k1 selects the part
-  a.sub_list = nullptr;                            // launch_fused: sticky queues
-  a.sub_list_off = nullptr;
+  a.sub_chunk_off = nullptr;                       // launch_fused: sticky queues
   a.sub_ctr = nullptr;
   a.sub_tiles = nullptr;
   a.n_sub = d.n_sub;
@@ -754,9 +752,8 @@ pinn_dd_status launch_fused(pinn_dd* h) {
   // the per-subdomain queues lose the global largest-first tail balance (C2
   // K1 1.345 -> 1.450 ms).
   static const bool no_sticky = std::getenv("PINN_DD_NO_STICKY") != nullptr;
-  if (!no_sticky && h->n_chunks1 >= 6 * h->grid1 && h->sub_list_tiles <= 2 * h->n_chunks1) {
-    a.sub_list = h->sub_list;
-    a.sub_list_off = h->sub_list_off;
+  if (!no_sticky && h->sticky_order && h->n_chunks1 >= 6 * h->grid1 && h->sub_list_tiles <= 2 * h->n_chunks1) {
+    a.sub_chunk_off = h->sub_chunk;
     a.sub_ctr = h->sub_ctr;
     a.sub_tiles = h->sub_tiles;
   }
@@ -993,8 +990,6 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   h->dgeo_local = reinterpret_cast<int32_t*>(base + L.dgeoloc);
   h->xflags = reinterpret_cast<unsigned long long*>(base + L.xflags);
   h->xstep = reinterpret_cast<int*>(base + L.xstep);
-  h->sub_list = reinterpret_cast<int32_t*>(base + L.slist);
-  h->sub_list_off = reinterpret_cast<int32_t*>(base + L.sloff);
   h->sub_ctr = reinterpret_cast<int32_t*>(base + L.sctr);
   h->sub_tiles = reinterpret_cast<int32_t*>(base + L.stiles);
 
@@ -1112,22 +1107,23 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   std::stable_sort(ord1.begin() + c1.size(), ord1.begin() + c1.size() + n_int, big_first);
   std::stable_sort(ord1.begin() + c1.size() + n_int, ord1.end(), big_first);
   h->n_int = n_int;
-  // per-subdomain queues of the fused step: residual + training chunks (big
-  // first), then interface chunks; cumulative tiles place the CTAs' first claims
-  std::vector<int32_t> slist, sloff(ns + 1, 0), stiles(ns + 1, 0);
+  // per-subdomain queues of the fused step: a subdomain's chunks in chunk
+  // order, which split_chunks makes residual + training chunks largest first,
+  // then interface chunks largest first (checked here; else no sticky queues);
+  // cumulative tiles place the CTAs' first claims
+  std::vector<int32_t> stiles(ns + 1, 0);
+  h->sticky_order = true;
   for (int q = 0; q < ns; ++q) {
-    sloff[q] = int32_t(slist.size());
-    std::vector<int32_t> in, itf;
-    for (int32_t i = subch[q]; i < subch[q + 1]; ++i) (c1[i].pad ? itf : in).push_back(i);
-    std::stable_sort(in.begin(), in.end(), big_first);
-    std::stable_sort(itf.begin(), itf.end(), big_first);
-    slist.insert(slist.end(), in.begin(), in.end());
-    slist.insert(slist.end(), itf.begin(), itf.end());
     int tiles = 0;
-    for (int32_t i = subch[q]; i < subch[q + 1]; ++i) tiles += (c1[i].count + P - 1) / P;
+    for (int32_t i = subch[q]; i < subch[q + 1]; ++i) {
+      tiles += (c1[i].count + P - 1) / P;
+      if (i > subch[q]) {
+        const Chunk &u = c1[i - 1], &v = c1[i];
+        if (u.pad > v.pad || (u.pad == v.pad && u.count < v.count)) h->sticky_order = false;
+      }
+    }
     stiles[q + 1] = stiles[q] + tiles;
   }
-  sloff[ns] = int32_t(slist.size());
   h->sub_list_tiles = stiles[ns];
   std::vector<int32_t> pm;
   h->ops->packmap(pm);
@@ -1167,8 +1163,6 @@ pinn_dd_status pinn_dd_create(const pinn_dd_desc* d, void* ws, size_t ws_bytes, 
   CKC(cudaMemcpyAsync(h->sub_adam, suba.data(), suba.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->chunks1, c1.data(), c1.size() * sizeof(Chunk), cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->order1, ord1.data(), ord1.size() * 4, cudaMemcpyHostToDevice, st));
-  CKC(cudaMemcpyAsync(h->sub_list, slist.data(), slist.size() * 4, cudaMemcpyHostToDevice, st));
-  CKC(cudaMemcpyAsync(h->sub_list_off, sloff.data(), sloff.size() * 4, cudaMemcpyHostToDevice, st));
   CKC(cudaMemcpyAsync(h->sub_tiles, stiles.data(), stiles.size() * 4, cudaMemcpyHostToDevice, st));
   CKC(cudaMemsetAsync(h->sub_ctr, 0, ns * 4, st));
   CKC(cudaMemsetAsync(h->sched, 0, 8 * sizeof(int32_t), st));

@@ -481,17 +481,33 @@ __device__ __forceinline__ int sticky_first_sub(const KArgs& a) {
   while (q + 1 < a.n_sub && a.sub_tiles[q + 1] <= target) ++q;
   return q;
 }
-__device__ __forceinline__ int sticky_claim(const KArgs& a, int& q, int& kq) {
+// Claim from the current queue (one atomic; its chunk range is cached in
+// st[4], st[5]), else scan the other queues in turn.  A queue's chunks are
+// contiguous in chunk order (sub_chunk_off), already largest first with the
+// interface chunks last, so the claimed place k IS chunk off + k.
+__device__ __forceinline__ int sticky_claim(const KArgs& a, volatile int* st) {
+  const int q = st[0];
+  if (q >= 0) {
+    const int k = atomicAdd(a.sub_ctr + q, 1);
+    if (k < st[5]) {
+      st[3] = k;
+      return st[4] + k;
+    }
+  }
+  const int q0 = q < 0 ? sticky_first_sub(a) : q + 1;
   for (int d = 0; d < a.n_sub; ++d) {
-    int qq = q + d;
+    int qq = q0 + d;
     if (qq >= a.n_sub) qq -= a.n_sub;
-    const int n = a.sub_list_off[qq + 1] - a.sub_list_off[qq];
+    if (qq == q) continue;   // just found empty
+    const int off = a.sub_chunk_off[qq], n = a.sub_chunk_off[qq + 1] - off;
     if (*reinterpret_cast<volatile int*>(a.sub_ctr + qq) >= n) continue;
     const int k = atomicAdd(a.sub_ctr + qq, 1);
     if (k < n) {
-      q = qq;
-      kq = k;
-      return a.sub_list[a.sub_list_off[qq] + k];
+      st[0] = qq;
+      st[3] = k;
+      st[4] = off;
+      st[5] = n;
+      return off + k;
     }
   }
   return -1;
@@ -502,7 +518,7 @@ __device__ __forceinline__ int sticky_claim(const KArgs& a, int& q, int& kq) {
 // (thread 0's state lives in shared memory: st[0] = current subdomain or -1
 // before the first claim, st[1] = 1 once the global payload queue is empty,
 // st[2] = a chunk claimed ahead (-1: none), st[3] = the current chunk's place
-// in its queue)
+// in its queue, st[4], st[5] = the queue's first chunk and length)
 __device__ __forceinline__ int next_item(const KArgs& a, int n_pay, volatile int* st) {
   if (st[2] >= 0) {
     const int c = st[2];
@@ -511,13 +527,10 @@ __device__ __forceinline__ int next_item(const KArgs& a, int n_pay, volatile int
   }
   if (st[1] == 0) {
     const int idx = atomicAdd(a.sched, 1);
-    if (a.sub_list == nullptr || idx < n_pay) return idx;
+    if (a.sub_chunk_off == nullptr || idx < n_pay) return idx;
     st[1] = 1;
   }
-  int q = st[0] < 0 ? sticky_first_sub(a) : st[0], kq = 0;
-  const int c = sticky_claim(a, q, kq);
-  st[0] = q;
-  st[3] = kq;
+  const int c = sticky_claim(a, st);
   return c < 0 ? a.n_chunks + n_pay : n_pay + c;
 }
 // Claim-ahead (thread 0, sticky phase; the TF32 kernel only -- the FP32 one
@@ -529,23 +542,19 @@ __device__ __forceinline__ int next_item(const KArgs& a, int n_pay, volatile int
 // into st[2] after the chunk.
 constexpr int kAheadMin = 16;
 __device__ __forceinline__ int sticky_ahead_issue(const KArgs& a, volatile int* st) {
-  if (a.sub_list == nullptr || st[1] == 0 || st[0] < 0) return -1;
-  const int q = st[0];
-  const int n = a.sub_list_off[q + 1] - a.sub_list_off[q];
-  if (st[3] + kAheadMin >= n) return -1;
-  return atomicAdd(a.sub_ctr + q, 1);
+  if (a.sub_chunk_off == nullptr || st[1] == 0 || st[0] < 0) return -1;
+  if (st[3] + kAheadMin >= st[5]) return -1;
+  return atomicAdd(a.sub_ctr + st[0], 1);
 }
 __device__ __forceinline__ void sticky_ahead_finish(const KArgs& a, volatile int* st, int k) {
   if (k < 0) return;
-  const int q = st[0];
-  const int n = a.sub_list_off[q + 1] - a.sub_list_off[q];
-  if (k < n) {
-    st[2] = a.sub_list[a.sub_list_off[q] + k];
+  if (k < st[5]) {
+    st[2] = st[4] + k;
     st[3] = k;
   }
 }
 __device__ __forceinline__ void sticky_reset(const KArgs& a) {
-  if (a.sub_list)
+  if (a.sub_chunk_off)
     for (int q = 0; q < a.n_sub; ++q) a.sub_ctr[q] = 0;
 }
 
@@ -713,7 +722,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
   const int xstep = px ? *reinterpret_cast<volatile int*>(a.px.step) : 0;
   const int64_t roff = px ? int64_t(xstep & 1) * a.px.n_recv : 0;
   if (tid < kMaxPeers) xcount[tid] = 0;
-  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::TOTAL - 6);   // sticky state [4] (next_item)
+  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::TOTAL - 6);   // sticky state [6] (next_item)
   if (tid == 0) {
     sst[0] = -1;
     sst[1] = 0;
@@ -729,7 +738,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
     if (idx >= a.n_chunks + n_pay) break;
     const bool pay = MODE == 1 || (MODE == 2 && idx < n_pay);   // payload chunk (forward + payload epilogue)
     const int li = idx - n_pay;
-    const bool direct = MODE == 2 && a.sub_list != nullptr;     // sticky: li is the chunk index
+    const bool direct = MODE == 2 && a.sub_chunk_off != nullptr;   // sticky: li is the chunk index
     const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (direct ? li : (a.order ? a.order[li] : li));
     const Chunk ch = (MODE == 2 && pay) ? a.chunks2[c] : a.chunks[c];
     if (MODE == 2 && !pay && ch.pad) {

@@ -229,7 +229,7 @@ struct TcCfg {
   static constexpr int oX = al4(oSl + NH);                   // [2][P]
   static constexpr int oU = oX + 2 * P;                      // [P][DO] float4
   static constexpr int oMisc = oU + 4 * P * DO;              // loss scratch [8][4], mbarrier, tmem slot, s_next
-  static constexpr int TOTAL = oMisc + 32 + 20;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts, sticky state
+  static constexpr int TOTAL = oMisc + 32 + 24;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts, sticky state
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget of the tensor-core kernel");
   static_assert((oH * 4) % 1024 == 0 && (oZ * 4) % 1024 == 0 && (WOPER * 4) % 1024 == 0, "operand alignment");
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   const int xstep = px ? *reinterpret_cast<volatile int*>(a.px.step) : 0;
   const int64_t roff = px ? int64_t(xstep & 1) * a.px.n_recv : 0;
   if (tid < kMaxPeers) xcount[tid] = 0;
-  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::oMisc + 46);   // sticky state (next_item)
+  volatile int* sst = reinterpret_cast<volatile int*>(sm + C::oMisc + 46);   // sticky state [6] (next_item)
   if (tid == 0) {
     sst[0] = -1;
     sst[1] = 0;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     if (idx >= a.n_chunks + n_pay) break;
     const bool pay = MODE == 1 || (MODE == 2 && idx < n_pay);
     const int li = idx - n_pay;
-    const bool direct = kSticky && a.sub_list != nullptr;   // sticky: li is the chunk index
+    const bool direct = kSticky && a.sub_chunk_off != nullptr;   // sticky: li is the chunk index
     const int c = pay ? (MODE == 2 ? idx : (a.order ? a.order[idx] : idx)) : (direct ? li : (a.order ? a.order[li] : li));
     const Chunk ch = (MODE == 2 && pay) ? a.chunks2[c] : a.chunks[c];
     if (MODE == 2 && !pay && ch.pad) {
