@@ -271,6 +271,11 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   int* xcount = reinterpret_cast<int*>(sm + C::oMisc + 38);    // [kMaxPeers] peer rows of a payload chunk
   const float m1 = a.m1, m2 = a.m2;
   const uint32_t aH = smem_u32(sH), aZ = smem_u32(sZ), aW = smem_u32(sW);
+#ifdef PINN_PHASE_PROF
+  long long prof_acc[20] = {};
+  long long prof_t0 = clock64();
+  int prof_cur = 0;
+#endif
 
   // ones column of H (bias of the forward MMA, db of the dW MMA): value rows 1,
   // derivative rows 0; columns 81..95 zero.  Activations write columns < 80 only.
@@ -326,6 +331,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
   }
 #pragma unroll 1
   for (;;) {
+    PROF_MARK(0);
     // The sticky schedule is compiled into the per-region-activation instance
     // only (C5: K1 0.324 -> 0.265 ms); in the 255-register 5x80 instance its
     // mere presence costs 9 % (C4 TF32 K1 5.61 -> 6.08 ms) and C4's big
@@ -347,6 +353,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     if (ch.sub != cur_sub) {
       // weights of subdomain ch.sub: W^k | b^k as tf32 operands, the rest FP32
       cta_sync();
+      PROF_MARK(1);
       const float* G = a.params + size_t(ch.sub) * a.pstride;
       for (int k = 2; k <= NH; ++k) {
         float* dst = sW + (k - 2) * WOPER;
@@ -363,6 +370,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       for (int e = tid; e < NH; e += T) sm[C::oSl + e] = a.slope_n * G[LY::offA(e + 1)];
       cur_sub = ch.sub;
     }
+    PROF_MARK(0);
     const int ahead = (kSticky && !pay && tid == 0) ? sticky_ahead_issue(a, sst) : -1;
     const float4 lw = a.sub_w[ch.sub];
     const int act = ACT == kActMixed ? a.sub_act[ch.sub] : ACT;
@@ -382,11 +390,13 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
         const int64_t p0 = int64_t(ch.start) + int64_t(t) * P;
         const int np = min(P, ch.count - t * P);
         const bool first = (t == 0);
+        PROF_MARK(MS == 1 ? 10 : 2);
         if (tid < P) {
           sX[tid] = tid < np ? a.coords[p0 + tid] : 0.0f;
           sY[tid] = tid < np ? a.coords[a.n_points + p0 + tid] : 0.0f;
         }
         cta_sync();
+        PROF_MARK(MS == 1 ? 10 : 3);
         // ---------------------------------------------------------- forward
         float4 z[kJT];
         {
@@ -409,10 +419,12 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
         for (int k = 2; k <= NH; ++k) {
           const uint32_t dcol = tm + uint32_t(80 * k);
           const uint32_t wk = aW + uint32_t((k - 2) * WOPER * 4);
+          PROF_MARK(MS == 1 ? 10 : 12);
           issue([&] {
 #pragma unroll 1
             for (int ks = 0; ks < KF / 8; ++ks) mma(dcol, kmajor(aH, ks), kmajor(wk, ks), idesc(M, N, 0, 0), ks > 0);
           });
+          PROF_MARK(MS == 1 ? 10 : 13);
           tload(tm, w, 80 * k, z);
           const float s = sSl[k - 1];
 #pragma unroll
@@ -422,6 +434,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
           if (k < NH) owrite(sH, w, z);   // the MMA that read H^{k-1} has completed
         }
+        PROF_MARK(MS == 1 ? 10 : 4);
         // z = H^NH of the thread's (point, 10 neurons).  Output layer on the CUDA
         // cores: partial dot products over the thread's neurons, combined over
         // the 4 lanes of a point (shuffles) and the two halves (shared memory).
@@ -445,6 +458,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           sU[e] = make_float4(u0.x + u1.x + sBo[e % DO], u0.y + u1.y, u0.z + u1.z, u0.w + u1.w);
         }
         cta_sync();
+        PROF_MARK(MS == 1 ? 11 : 5);
         // --------------------------------------------------------- epilogue
         if constexpr (MS == 1) {
           for (int p = tid; p < np; p += T) {
@@ -467,6 +481,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             for (int o = 0; o < DO; ++o) sU[p * DO + o] = Ub[o];
           }
           cta_sync();
+          PROF_MARK(6);
           // ------------------------------------------------------- reverse
           // output layer: Hb^NH = W^L^T Ub (thread-local); dW^L[o][j] =
           // sum_p Ub[p][o] . H^NH[p][j] (4 channels), db^L = sum_p Ub_value
@@ -544,6 +559,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           };
 #pragma unroll 1
           for (int k = NH; k >= 2; --k) {
+            PROF_MARK(15);
             tload(tm, w, 80 * k, z);
             {
               const float s = sSl[k - 1];
@@ -556,10 +572,13 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
 #pragma unroll
               for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
             }
+            PROF_MARK(16);
             flush_dw();   // the previous dW MMA has read Zb / H: they may be overwritten
+            PROF_MARK(17);
             owrite(sZ, w, hb);   // Zb^k
             owrite(sH, w, z);    // H^{k-1}
             const uint32_t wk = aW + uint32_t((k - 2) * WOPER * 4);
+            PROF_MARK(18);
             fence_async_smem();
             tmem_fence_before();
             cta_sync();
@@ -580,9 +599,12 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             mbar_wait(mbar, phase);
             phase ^= 1u;
             tmem_fence_after();
+            PROF_MARK(19);
             tload(tm, w, 0, hb);   // Hb^{k-1} from R
           }
+          PROF_MARK(16);
           flush_dw();
+          PROF_MARK(8);
           // layer 1: Zb^1 = act_bwd(S_1, Hb^1); dW^1[j] = sum_p (zb_v x_p + zb_{d_i}), db^1 = sum_p zb_v
           tload(tm, w, 80, z);
           {
@@ -620,6 +642,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           cta_sync();
         }
       }
+      PROF_MARK(9);
       if constexpr (MS == 0) {
         if (ntiles > 0) {
           block_sum<4, T>(lsum, sLoss);
@@ -661,6 +684,15 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     if (kSticky && tid == 0) sticky_ahead_finish(a, sst, ahead);
     cta_sync();
   }
+#ifdef PINN_PHASE_PROF
+  PROF_MARK(0);
+  if (tid == 0 && blockIdx.x < 4)
+    printf("PHASE N=%d NH=%d MODE=%d cta=%d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld "
+           "%lld %lld %lld %lld %lld\n", N, NH, MODE, int(blockIdx.x), prof_acc[0], prof_acc[1], prof_acc[2],
+           prof_acc[3], prof_acc[4], prof_acc[5], prof_acc[6], prof_acc[7], prof_acc[8], prof_acc[9], prof_acc[10],
+           prof_acc[11], prof_acc[12], prof_acc[13], prof_acc[14], prof_acc[15], prof_acc[16], prof_acc[17],
+           prof_acc[18], prof_acc[19]);
+#endif
   if (tid == 0) {
     __threadfence();
     if (atomicAdd(a.sched + 1, 1) == int(gridDim.x) - 1) {
