@@ -229,7 +229,7 @@ struct TcCfg {
   static constexpr int oX = al4(oSl + NH);                   // [2][P]
   static constexpr int oU = oX + 2 * P;                      // [P][DO] float4
   static constexpr int oMisc = oU + 4 * P * DO;              // loss scratch [8][4], mbarrier, tmem slot, s_next
-  static constexpr int TOTAL = oMisc + 32 + 24;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts, sticky state
+  static constexpr int TOTAL = oMisc + 32 + 28;  // loss scratch, 2 mbarriers, tmem slot, s_next, peer counts, sticky state
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= 227 * 1024, "shared memory budget of the tensor-core kernel");
   static_assert((oH * 4) % 1024 == 0 && (oZ * 4) % 1024 == 0 && (WOPER * 4) % 1024 == 0, "operand alignment");
@@ -312,6 +312,55 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     mbar_wait(mbar, phase);
     phase ^= 1u;
     tmem_fence_after();
+  };
+
+  // Deferred dW flush.  The reverse step of layer k leaves dW^k^T in S_k's
+  // columns (lanes i, columns j); it is added into its chunk's partial only
+  // when S_k is next needed -- inside the next tile's forward pass, while the
+  // MMA of layer k - 1 runs (the threads would otherwise idle in its wait).
+  // State (uniform, in shared memory): the pending layer mask, the partial
+  // and whether that tile was its chunk's first (store instead of add).
+  volatile int* dpend = reinterpret_cast<volatile int*>(sm + C::oMisc + 52);
+  volatile int* dfirst = reinterpret_cast<volatile int*>(sm + C::oMisc + 53);
+  float* volatile* dpc = reinterpret_cast<float* volatile*>(sm + C::oMisc + 54);
+  if (tid == 0) *dpend = 0;
+  // add dW^k^T (pending in S_k) into the partial; every thread reads the
+  // state before anyone can change it (callers sit between CTA barriers)
+  auto flush_layer = [&](int k) {
+    float* P0 = *dpc;
+    const bool fst = *dfirst != 0;
+    if (w.q < 3) {   // lanes i = 0..95 (i < 80: W^k column i; i = 80: b^k)
+      uint32_t r[5][8];
+#pragma unroll
+      for (int b = 0; b < 5; ++b)
+        ld32x8(tm + (uint32_t(32 * w.q) << 16) + uint32_t(80 * k + 40 * w.hf + 8 * b), r[b]);
+      ld_wait();
+      const int i = 32 * w.q + (tid & 31);
+      if (i <= N) {
+        float* g = i < N ? P0 + LY::offW(k) + 40 * w.hf * N + i : P0 + LY::offB(k) + 40 * w.hf;
+        const int st = i < N ? N : 1;
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float* gp = g + (8 * b + e) * st;
+            if (fst)
+              *gp = __uint_as_float(r[b][e]);
+            else
+              red_add(gp, __uint_as_float(r[b][e]));
+          }
+      }
+    }
+  };
+  auto flush_pending = [&](int k) {   // flush layer k if pending (uniform branch)
+    if (*dpend & (1 << k)) {
+      flush_layer(k);
+      tmem_fence_before();
+      cta_sync();
+      if (tid == 0) *dpend = *dpend & ~(1 << k);
+      cta_sync();
+      tmem_fence_after();
+    }
   };
 
   int cur_sub = -1;
@@ -415,15 +464,36 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
           owrite(sH, w, z);
         }
+        flush_pending(2);   // S_2 is written by the first forward MMA
 #pragma unroll 1
         for (int k = 2; k <= NH; ++k) {
           const uint32_t dcol = tm + uint32_t(80 * k);
           const uint32_t wk = aW + uint32_t((k - 2) * WOPER * 4);
           PROF_MARK(MS == 1 ? 10 : 12);
-          issue([&] {
-#pragma unroll 1
+          // issue MMA(k); while it runs, flush S_{k+1} (dW^{k+1} of the previous tile)
+          fence_async_smem();
+          tmem_fence_before();
+          cta_sync();
+          const int pend_next = (k < NH) ? (*dpend & (1 << (k + 1))) : 0;
+          if (tid == 0) {
+            tmem_fence_after();
+#pragma unroll
             for (int ks = 0; ks < KF / 8; ++ks) mma(dcol, kmajor(aH, ks), kmajor(wk, ks), idesc(M, N, 0, 0), ks > 0);
-          });
+            commit(mbar);
+          }
+          if (pend_next) {
+            tmem_fence_after();
+            flush_layer(k + 1);
+          }
+          mbar_wait(mbar, phase);
+          phase ^= 1u;
+          tmem_fence_after();
+          if (pend_next) {
+            tmem_fence_before();
+            cta_sync();   // every thread has read the state and S_{k+1} (tcgen05.wait::ld)
+            if (tid == 0) *dpend = *dpend & ~(1 << (k + 1));
+            tmem_fence_after();
+          }
           PROF_MARK(MS == 1 ? 10 : 13);
           tload(tm, w, 80 * k, z);
           const float s = sSl[k - 1];
@@ -527,34 +597,18 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           // Hb^{k-1} and compute the next step's activation maps; its result
           // (dW^k^T in S_k: lanes i, columns j) is added to the chunk partial
           // just before the next operands overwrite its inputs.
-          int pend = 0;   // layer whose dW^T waits in TMEM (0 = none)
-          auto flush_dw = [&]() {
+          // this tile's dW^k^T stay in S_k after their MMAs (deferred flush; the
+          // forward pass has flushed every earlier one, so dpend == 0 here)
+          if (tid == 0) {
+            *dpc = Pc;
+            *dfirst = first ? 1 : 0;
+          }
+          int pend = 0;   // layer whose dW MMA may still be reading Zb / H (0 = none)
+          auto wait_dw = [&]() {
             if (!pend) return;
             mbar_wait(mbar2, phase2);
             phase2 ^= 1u;
             tmem_fence_after();
-            if (w.q < 3) {   // lanes i = 0..95 (i < 80: W^k column i; i = 80: b^k)
-              uint32_t r[5][8];
-#pragma unroll
-              for (int b = 0; b < 5; ++b)
-                ld32x8(tm + (uint32_t(32 * w.q) << 16) + uint32_t(80 * pend + 40 * w.hf + 8 * b), r[b]);
-              ld_wait();
-              const int i = 32 * w.q + (tid & 31);
-              if (i <= N) {
-                float* g = i < N ? Pc + LY::offW(pend) + 40 * w.hf * N + i : Pc + LY::offB(pend) + 40 * w.hf;
-                const int st = i < N ? N : 1;
-#pragma unroll
-                for (int b = 0; b < 5; ++b)
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) {
-                    float* gp = g + (8 * b + e) * st;
-                    if (first)
-                      *gp = __uint_as_float(r[b][e]);
-                    else
-                      red_add(gp, __uint_as_float(r[b][e]));
-                  }
-              }
-            }
             pend = 0;
           };
 #pragma unroll 1
@@ -573,7 +627,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
               for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
             }
             PROF_MARK(16);
-            flush_dw();   // the previous dW MMA has read Zb / H: they may be overwritten
+            wait_dw();   // the previous dW MMA has read Zb / H: they may be overwritten
             PROF_MARK(17);
             owrite(sZ, w, hb);   // Zb^k
             owrite(sH, w, z);    // H^{k-1}
@@ -594,6 +648,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
               for (int ks = 0; ks < M / 8; ++ks)
                 mma(tm + uint32_t(80 * k), mnmajor(aH, ks), mnmajor(aZ, ks), idesc(M, N, 1, 1), ks > 0);
               commit(mbar2);
+              *dpend = *dpend | (1 << k);
             }
             pend = k;
             mbar_wait(mbar, phase);
@@ -603,7 +658,7 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             tload(tm, w, 0, hb);   // Hb^{k-1} from R
           }
           PROF_MARK(16);
-          flush_dw();
+          wait_dw();
           PROF_MARK(8);
           // layer 1: Zb^1 = act_bwd(S_1, Hb^1); dW^1[j] = sum_p (zb_v x_p + zb_{d_i}), db^1 = sum_p zb_v
           tload(tm, w, 80, z);
@@ -684,6 +739,8 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
     if (kSticky && tid == 0) sticky_ahead_finish(a, sst, ahead);
     cta_sync();
   }
+  // the last tile's dW (pending in S_k)
+  for (int k = 2; k <= NH; ++k) flush_pending(k);
 #ifdef PINN_PHASE_PROF
   PROF_MARK(0);
   if (tid == 0 && blockIdx.x < 4)
