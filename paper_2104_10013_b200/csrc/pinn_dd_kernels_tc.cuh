@@ -449,6 +449,13 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       constexpr int AS = decltype(act_c)::value;
       constexpr int MS = decltype(mode_c)::value;   // 0 loss + gradient, 1 payload
       float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      // coordinates of the next tile are loaded into registers while the
+      // current tile computes (thread p < P owns point p of a tile)
+      float cx = 0.0f, cy = 0.0f;
+      if (tid < min(P, ch.count)) {
+        cx = a.coords[int64_t(ch.start) + tid];
+        cy = a.coords[a.n_points + int64_t(ch.start) + tid];
+      }
 #pragma unroll 1
       for (int t = 0; t < ntiles; ++t) {
         const int64_t p0 = int64_t(ch.start) + int64_t(t) * P;
@@ -456,8 +463,13 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
         const bool first = (t == 0);
         PROF_MARK(MS == 1 ? 10 : 2);
         if (tid < P) {
-          sX[tid] = tid < np ? a.coords[p0 + tid] : 0.0f;
-          sY[tid] = tid < np ? a.coords[a.n_points + p0 + tid] : 0.0f;
+          sX[tid] = cx;
+          sY[tid] = cy;
+          cx = cy = 0.0f;
+          if (t + 1 < ntiles && tid < min(P, ch.count - (t + 1) * P)) {
+            cx = a.coords[p0 + P + tid];
+            cy = a.coords[a.n_points + p0 + P + tid];
+          }
         }
         cta_sync();
         PROF_MARK(MS == 1 ? 10 : 3);
