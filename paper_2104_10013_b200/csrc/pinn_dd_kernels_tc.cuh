@@ -404,27 +404,26 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       cta_sync();
       PROF_MARK(1);
       const float* G = a.params + size_t(ch.sub) * a.pstride;
-      // batches of 8 loads in flight per thread: a one-at-a-time loop cannot
-      // move a load above the previous (generic-pointer) shared store, which
-      // made a reload ~110 serial L2 round trips (4.5 % of C4's TF32 K1)
+      // every load of a layer in flight before its stores (a one-at-a-time loop
+      // cannot move a load above the previous generic-pointer shared store,
+      // which made a reload ~110 serial L2 round trips: 4.5 % of C4's TF32 K1)
+      constexpr int WIT = (N * CP + T - 1) / T;
+#pragma unroll 1
       for (int k = 2; k <= NH; ++k) {
         float* dst = sW + (k - 2) * WOPER;
-#pragma unroll 1
-        for (int e0 = tid; e0 < N * CP; e0 += 8 * T) {
-          float v[8];
+        float v[WIT];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + u * T;
-            const int j = e / CP, i = e % CP;
-            v[u] = e >= N * CP ? 0.0f
-                               : (i < N ? __ldcg(G + LY::offW(k) + j * N + i)
-                                        : (i == N ? __ldcg(G + LY::offB(k) + j) : 0.0f));
-          }
+        for (int u = 0; u < WIT; ++u) {
+          const int e = tid + u * T;
+          const int j = e / CP, i = e % CP;
+          v[u] = e >= N * CP ? 0.0f
+                             : (i < N ? __ldcg(G + LY::offW(k) + j * N + i)
+                                      : (i == N ? __ldcg(G + LY::offB(k) + j) : 0.0f));
+        }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + u * T;
-            if (e < N * CP) dst[sw32(e / CP, e % CP)] = to_tf32(v[u]);
-          }
+        for (int u = 0; u < WIT; ++u) {
+          const int e = tid + u * T;
+          if (e < N * CP) dst[sw32(e / CP, e % CP)] = to_tf32(v[u]);
         }
       }
       float* s1 = sm + C::oW1;
