@@ -490,38 +490,38 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
           owrite(sH, w, z);
         }
-        flush_pending(2);   // S_2 is written by the first forward MMA
 #pragma unroll 1
         for (int k = 2; k <= NH; ++k) {
-          const uint32_t dcol = tm + uint32_t(80 * k);
           const uint32_t wk = aW + uint32_t((k - 2) * WOPER * 4);
           PROF_MARK(MS == 1 ? 10 : 12);
-          // issue MMA(k); while it runs, flush S_{k+1} (dW^{k+1} of the previous tile)
+          // MMA(k) into R (free during the forward pass); while it runs, add
+          // the previous tile's dW^k (pending in S_k) into its chunk partial,
+          // then the stash form of layer k goes into S_k
           fence_async_smem();
           tmem_fence_before();
           cta_sync();
-          const int pend_next = (k < NH) ? (*dpend & (1 << (k + 1))) : 0;
+          const int pend_k = (MS == 0) ? (*dpend & (1 << k)) : 0;
           if (tid == 0) {
             tmem_fence_after();
 #pragma unroll
-            for (int ks = 0; ks < KF / 8; ++ks) mma(dcol, kmajor(aH, ks), kmajor(wk, ks), idesc(M, N, 0, 0), ks > 0);
+            for (int ks = 0; ks < KF / 8; ++ks) mma(tm, kmajor(aH, ks), kmajor(wk, ks), idesc(M, N, 0, 0), ks > 0);
             commit(mbar);
           }
-          if (pend_next) {
+          if (pend_k) {
             tmem_fence_after();
-            flush_layer(k + 1);
+            flush_layer(k);
           }
           mbar_wait(mbar, phase);
           phase ^= 1u;
           tmem_fence_after();
-          if (pend_next) {
+          if (pend_k) {
             tmem_fence_before();
-            cta_sync();   // every thread has read the state and S_{k+1} (tcgen05.wait::ld)
-            if (tid == 0) *dpend = *dpend & ~(1 << (k + 1));
+            cta_sync();   // every thread has read the state and S_k (tcgen05.wait::ld)
+            if (tid == 0) *dpend = *dpend & ~(1 << k);
             tmem_fence_after();
           }
           PROF_MARK(MS == 1 ? 10 : 13);
-          tload(tm, w, 80 * k, z);
+          tload(tm, w, 0, z);
           const float s = sSl[k - 1];
 #pragma unroll
           for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
