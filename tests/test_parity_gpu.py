@@ -384,6 +384,34 @@ def test_fused_step_equals_phased_calls(cfg, kw):
     b.close()
 
 
+@pytest.mark.parametrize("tf32", [False, True])
+def test_sticky_schedule_fused_step_equals_phased_calls(tf32):
+    """Full-size C5 (one-tile chunks, > 6 per CTA) runs the fused step on the
+    sticky per-subdomain queues (the TF32 instance also claims
+    ahead), while loss_grad runs the global largest-first queue: losses,
+    gradient-driven Adam update and parameters are bitwise equal, i.e. the
+    schedule never changes a result."""
+    from paper_2104_10013_b200.binding import FLAG_GRAPH, FLAG_TF32
+    prob = make_config("C5")
+    fl = FLAG_GRAPH | (FLAG_TF32 if tf32 else 0)
+    a = _handle(prob, flags=fl)
+    assert a.step_fused
+    info = a.plan_info()
+    assert info[2] >= 6 * info[3], info           # the sticky-queue regime
+    out = a.step(1)
+    b = _handle(prob, flags=fl)
+    b.interface_payload()
+    lb, gb = b.loss_grad()
+    b.adam()
+    torch.cuda.synchronize()
+    for q in range(prob.n_sub):
+        assert np.array_equal(np.asarray(out[q, :5]), lb[q, :5].cpu().numpy()), q
+        assert torch.equal(a.get(q, 3), b.get(q, 3)), q
+        assert torch.equal(a.get(q, 0), b.get(q, 0)), q
+    a.close()
+    b.close()
+
+
 def test_read_loss_async_matches_step_loss():
     """pinn_dd_read_loss (stream-ordered, no sync) into pinned host and device
     tensors returns the breakdown pinn_dd_step reports."""
