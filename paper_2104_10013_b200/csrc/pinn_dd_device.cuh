@@ -116,7 +116,10 @@ struct KCfg {
   static constexpr int ACC = Lay<N, NH, DO>::total();
   // scratch: split s holds dW^k as [j][N + 1] (row padding spreads the dW-block
   // writers over the banks; readers walk rows contiguously) then db^k [N]
-  static constexpr int SROW = N + 1;
+  // row stride of the split scratch: N + 1 spreads the 16 x 2 / 4 x 8 (width
+  // 40: 8 x 4 with NJ = 8 -> stride 41) dW-block writers over the banks; for
+  // width 80's 8 x 4 warp blocks, 84 (= 20 mod 32) does
+  static constexpr int SROW = N == 80 ? N + 4 : N + 1;
   static constexpr int SSPL = N * SROW;                    // floats per split (W part)
   static constexpr int SCR1 = S * SSPL + S * N;
   static constexpr bool DW_SMEM = (size_t(al4(al4(oDw + (S > 1 ? SCR1 : 0)) + ACC + 4)) * 4) <= SMEM_CAP;

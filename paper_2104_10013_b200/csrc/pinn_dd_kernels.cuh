@@ -227,7 +227,12 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
   const int tid = threadIdx.x;
   if (tid < NBLK * S) {
     const int r = tid % NBLK, s = tid / NBLK;
-    const int jb = r % NJ, ib = r / NJ;   // a warp covers 8 row blocks x 4 column blocks
+    // a warp covers 8 row blocks x 4 column blocks: its Zb row loads are 8
+    // distinct float4 (one wavefront) and its H loads 4 (broadcast).  For
+    // NJ = 16 (width 80) the plain r % NJ split gave 16 x 2 per warp (two
+    // wavefronts per Zb load: 15 instead of 10 per point and warp)
+    const int jb = NJ == 16 ? ((r & 7) | (((r >> 5) & 1) << 3)) : r % NJ;
+    const int ib = NJ == 16 ? (((r >> 3) & 3) | ((r >> 6) << 2)) : r / NJ;
     float2 acc2[JB][IB];   // (x.x + z.z, y.y + w.w) channel pairs, one FFMA2 each
     float db[JB];
 #pragma unroll
