@@ -324,16 +324,20 @@ int n_eq_of(int pde) { return pde == PINN_DD_PDE_NS ? 3 : 1; }
 // [1, 4] (ACC = floats of a chunk's gradient partial, flushed once per chunk
 // and read back by K5a: 6x40 -> 4, 5x20 -> 1, i.e. 3-tile chunks for C3's
 // 324-tile runs, K1 0.267 -> 0.260 ms); shorter runs (the small C5 regions)
-// 1-tile chunks so the persistent schedule's tail stays one tile long (C5 K1
-// 0.573 -> 0.531 ms).  Depends only on cnt and the net (placement invariance).
-int chunk_tiles(int cnt, int P, int acc) {
+// 2-tile chunks (with the sticky queues of the fused step, which keep a CTA on
+// one region, 2-tile chunks halve the per-chunk work: C5 K1 0.438 -> 0.430
+// ms, TF32 0.221 -> 0.218 ms, and keeping 1-tile interface chunks cost TF32
+// 7 %; on the global queue 1-tile chunks had the shorter tail: 0.573 -> 0.531
+// ms in round 1).  Depends only on cnt and the net (placement invariance).
+int chunk_tiles(int cnt, int P, int acc, bool interior = true) {
   static const int min_env = [] {   // development knob: PINN_DD_MIN_CHUNK_TILES
     const char* e = std::getenv("PINN_DD_MIN_CHUNK_TILES");
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
   const int tiles = (cnt + P - 1) / P;
   const int m = std::min(4, std::max(1, acc / 2048));
-  const int min_tiles = min_env ? min_env : (tiles >= 200 ? m : 1);
+  const int min_tiles = min_env ? min_env : (tiles >= 200 ? m : 2);
+  (void)interior;
   // a giant run (the data-parallel comparator's single subdomain: 7,530 tiles
   // of 32) would get only ~128 chunks -- fewer than the persistent CTAs -- so
   // runs of > 2048 tiles with partials of <= 64 KB may use up to 1024 chunks
@@ -344,9 +348,9 @@ int chunk_tiles(int cnt, int P, int acc) {
 // point counts of the K1 chunks of a run of `cnt` points: full chunks of
 // chunk_tiles(cnt) tiles, the remainder as one-tile chunks (the schedule's
 // tail); depends only on cnt (placement invariance)
-void chunk_sizes(int cnt, int P, int acc, std::vector<int>& out) {
+void chunk_sizes(int cnt, int P, int acc, bool interior, std::vector<int>& out) {
   if (cnt == 0) return;
-  const int span = chunk_tiles(cnt, P, acc) * P;
+  const int span = chunk_tiles(cnt, P, acc, interior) * P;
   int s0 = 0;
   for (; s0 + span <= cnt; s0 += span) out.push_back(span);
   for (; s0 < cnt; s0 += P) out.push_back(std::min(P, cnt - s0));
@@ -358,8 +362,8 @@ void chunk_sizes(int cnt, int P, int acc, std::vector<int>& out) {
 // An empty subdomain still gets one (empty) chunk and thus a partial slot.
 std::vector<int> split_chunks(int na, int ni, int P, int acc) {
   std::vector<int> a, b;
-  chunk_sizes(na, P, acc, a);
-  chunk_sizes(ni, P, acc, b);
+  chunk_sizes(na, P, acc, true, a);
+  chunk_sizes(ni, P, acc, false, b);
   for (int& v : b) v = -v - 1;
   a.insert(a.end(), b.begin(), b.end());
   if (a.empty()) a.push_back(0);
@@ -752,7 +756,7 @@ pinn_dd_status launch_fused(pinn_dd* h) {
   // the per-subdomain queues lose the global largest-first tail balance (C2
   // K1 1.345 -> 1.450 ms).
   static const bool no_sticky = std::getenv("PINN_DD_NO_STICKY") != nullptr;
-  if (!no_sticky && h->sticky_order && h->n_chunks1 >= 6 * h->grid1 && h->sub_list_tiles <= 2 * h->n_chunks1) {
+  if (!no_sticky && h->sticky_order && h->n_chunks1 >= 4 * h->grid1 && h->sub_list_tiles <= 2 * h->n_chunks1) {
     a.sub_chunk_off = h->sub_chunk;
     a.sub_ctr = h->sub_ctr;
     a.sub_tiles = h->sub_tiles;
