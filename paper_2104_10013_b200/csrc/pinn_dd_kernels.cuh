@@ -298,29 +298,37 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 // Global chunk partial (!DWS) with few entries per thread: its current values
 // are loaded right after gemm_dw (before gemm_bwd and the barrier), so the L2
 // round trip overlaps the input-adjoint GEMM instead of following the barrier.
-// db^k[j] = sum_p Zb^k[j][p].value for thread j < N (4 interleaved chains,
-// combined in fixed order).  Called after the input-adjoint GEMM and before
-// the barrier that precedes the next writes of the Zb buffer.
+// db^k[j] = sum_p Zb^k[j][p].value, written to the scratch's db slot
+// sDw[DBOFF + j] for gemm_dw_reduce (after the next barrier).  TPR threads per
+// row (consecutive lanes), each 4 interleaved chains over every TPR-th point,
+// combined in a fixed order (chains, then an xor-shuffle tree): width 20 puts
+// 80 threads on 20 rows of 64 points instead of 20 threads on 64 each.
+// Called after the input-adjoint GEMM and before the barrier that precedes
+// the next writes of the Zb buffer.
 template <int N, int NH, int DO, int T, bool DWS>
-__device__ __forceinline__ float db_sum(const float4* __restrict__ Zb) {
+__device__ __forceinline__ void db_sum(const float4* __restrict__ Zb, float* sDw) {
   using C = KCfg<N, NH, DO, T>;
-  if constexpr (C::S == 1 && DWS) {
-    return 0.0f;   // gemm_dw accumulates db itself on this path
-  } else {
-    static_assert(C::P % 4 == 0, "four chains");
+  if constexpr (!(C::S == 1 && DWS)) {   // else gemm_dw accumulates db itself
+    constexpr int TPR = (N * 4 <= T && C::P % 16 == 0) ? 4 : ((N * 2 <= T && C::P % 8 == 0) ? 2 : 1);
+    static_assert(C::P % (4 * TPR) == 0, "four chains per thread");
+    constexpr int DBOFF = C::S * C::SSPL;
     const int tid = threadIdx.x;
+    const int j = tid / TPR, sub = tid % TPR;
     float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-    if (tid < N) {
-      const float4* z = Zb + C::row(tid);
-#pragma unroll 8
-      for (int p = 0; p < C::P; p += 4) {
+    if (j < N) {
+      const float4* z = Zb + C::row(j);
+#pragma unroll
+      for (int p = sub; p < C::P; p += 4 * TPR) {
         a0 += z[p].x;
-        a1 += z[p + 1].x;
-        a2 += z[p + 2].x;
-        a3 += z[p + 3].x;
+        a1 += z[p + TPR].x;
+        a2 += z[p + 2 * TPR].x;
+        a3 += z[p + 3 * TPR].x;
       }
     }
-    return (a0 + a1) + (a2 + a3);
+    float v = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 1; o < TPR; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (j < N && sub == 0) sDw[DBOFF + j] = v;
   }
 }
 
@@ -347,7 +355,7 @@ __device__ __forceinline__ void gemm_dw_prefetch(const float* accW, const float*
 
 template <int N, int NH, int DO, int T, bool DWS>
 __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool first, const float* sDw,
-                                               const float* pre, float preb, float dbv) {
+                                               const float* pre, float preb) {
   using C = KCfg<N, NH, DO, T>;
   constexpr int S = C::S;
   constexpr bool PRE = DwPre<N, NH, DO, T, DWS>::ON;
@@ -386,7 +394,7 @@ __device__ __forceinline__ void gemm_dw_reduce(float* accW, float* accB, bool fi
       if (e < NE) accW[e] = (DWS || !first) ? cur[it] + v[it] : v[it];
     }
     if (tid < N) {
-      const float x = dbv;   // db_sum
+      const float x = sDw[S * C::SSPL + tid];   // db_sum
       if constexpr (PRE)
         accB[tid] = first ? x : preb + x;
       else
@@ -995,11 +1003,11 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
                 for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
               });
             }
-            const float dbv = db_sum<N, NH, DO, T, DSM>(bufZ);
+            db_sum<N, NH, DO, T, DSM>(bufZ, sDw);
             PROF_MARK(18);
             cta_sync();
             PROF_MARK(19);
-            gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw, pre, preb, dbv);
+            gemm_dw_reduce<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, sDw, pre, preb);
 #pragma unroll
             for (int jj = 0; jj < kJT; ++jj) {
               bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
