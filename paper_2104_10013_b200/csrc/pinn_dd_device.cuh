@@ -127,7 +127,13 @@ struct KCfg {
   // accumulator in global memory, to coalesce the per-tile read-modify-write
   static constexpr int SCR = (S > 1 || !DW_SMEM) ? SCR1 : 0;
   static constexpr int oAcc = al4(oDw + SCR);              // per-chunk gradient accumulator
-  static constexpr int TOTAL = al4(oAcc + (DW_SMEM ? ACC : 0) + 16);  // + peer row counts [8], tmem slot, s_next, sticky state [4]
+  // a third activation buffer (widths <= 40, where it fits): the reverse
+  // sweep then reads each stash slot from TMEM once (its raw jets stay in
+  // registers for the next step's act_bwd; the recomputed activation goes
+  // straight into the free buffer) instead of twice
+  static constexpr int oBuf3 = al4(oAcc + (DW_SMEM ? ACC : 0));
+  static constexpr bool BUF3 = N <= 40 && size_t(al4(oBuf3 + BUF + 16)) * 4 <= SMEM_CAP;
+  static constexpr int TOTAL = al4(oBuf3 + (BUF3 ? BUF : 0) + 16);  // + peer row counts [8], tmem slot, s_next, sticky state [4]
   static constexpr size_t SMEM = size_t(TOTAL) * 4;
   static_assert(SMEM <= SMEM_CAP, "shared memory budget");
   static_assert(NBLK * S <= T, "dW blocks per CTA");

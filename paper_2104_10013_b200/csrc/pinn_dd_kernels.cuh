@@ -234,10 +234,8 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
     const int jb = NJ == 16 ? ((r & 7) | (((r >> 5) & 1) << 3)) : r % NJ;
     const int ib = NJ == 16 ? (((r >> 3) & 3) | ((r >> 6) << 2)) : r / NJ;
     float2 acc2[JB][IB];   // (x.x + z.z, y.y + w.w) channel pairs, one FFMA2 each
-    float db[JB];
 #pragma unroll
     for (int jj = 0; jj < JB; ++jj) {
-      db[jj] = 0.0f;
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc2[jj][ii] = make_float2(0.0f, 0.0f);
     }
@@ -255,10 +253,6 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
           acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].x, zr[jj].y), make_float2(hr[ii].x, hr[ii].y), acc2[jj][ii]);
           acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].z, zr[jj].w), make_float2(hr[ii].z, hr[ii].w), acc2[jj][ii]);
         }
-      if constexpr (S == 1 && DWS) {
-#pragma unroll
-        for (int jj = 0; jj < JB; ++jj) db[jj] += zr[jj].x;
-      }
     }
     float acc[JB][IB];
 #pragma unroll
@@ -267,18 +261,16 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
       for (int ii = 0; ii < IB; ++ii) acc[jj][ii] = acc2[jj][ii].x + acc2[jj][ii].y;
     if constexpr (S == 1 && DWS) {
       // shared chunk accumulator, entries private to this thread: loads first
-      float cur[JB][IB], curb[JB];
+      float cur[JB][IB];
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj) {
 #pragma unroll
         for (int ii = 0; ii < IB; ++ii) cur[jj][ii] = accW[(jb + NJ * jj) * N + ib + NI * ii];
-        curb[jj] = ib == 0 ? accB[jb + NJ * jj] : 0.0f;
       }
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj) {
 #pragma unroll
         for (int ii = 0; ii < IB; ++ii) accW[(jb + NJ * jj) * N + ib + NI * ii] = cur[jj][ii] + acc[jj][ii];
-        if (ib == 0) accB[jb + NJ * jj] = curb[jj] + db[jj];
       }
     } else {
       // db^k is summed once per row by db_sum (the NI threads of a row block
@@ -306,9 +298,9 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 // Called after the input-adjoint GEMM and before the barrier that precedes
 // the next writes of the Zb buffer.
 template <int N, int NH, int DO, int T, bool DWS>
-__device__ __forceinline__ void db_sum(const float4* __restrict__ Zb, float* sDw) {
+__device__ __forceinline__ void db_sum(const float4* __restrict__ Zb, float* sDw, float* accB) {
   using C = KCfg<N, NH, DO, T>;
-  if constexpr (!(C::S == 1 && DWS)) {   // else gemm_dw accumulates db itself
+  {
     constexpr int TPR = (N * 4 <= T && C::P % 16 == 0) ? 4 : ((N * 2 <= T && C::P % 8 == 0) ? 2 : 1);
     static_assert(C::P % (4 * TPR) == 0, "four chains per thread");
     constexpr int DBOFF = C::S * C::SSPL;
@@ -328,7 +320,12 @@ __device__ __forceinline__ void db_sum(const float4* __restrict__ Zb, float* sDw
     float v = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 1; o < TPR; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (j < N && sub == 0) sDw[DBOFF + j] = v;
+    if (j < N && sub == 0) {
+      if constexpr (C::S == 1 && DWS)
+        accB[j] += v;   // the chunk's shared accumulator (gemm_dw_reduce is empty on this path)
+      else
+        sDw[DBOFF + j] = v;
+    }
   }
 }
 
@@ -956,23 +953,37 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
               for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
             });
             if (NH >= 2) {
-              st.load(NH - 2, reinterpret_cast<float*>(z));
-              const float s2 = sSl[NH - 2];
-              with_act<ACT>(act, [&](auto act_c) {
-                constexpr int AS = decltype(act_c)::value;
+              st.load(NH - 2, reinterpret_cast<float*>(z));   // BUF3: stays raw (layer NH - 1's jets)
+              if constexpr (!C::BUF3) {
+                const float s2 = sSl[NH - 2];
+                with_act<ACT>(act, [&](auto act_c) {
+                  constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-                for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
-              });
+                  for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+                });
+              }
             }
           }
           float4* bufZ = buf0;   // adjoint of the current layer's pre-activation
           float4* bufH = buf1;   // activation of the layer below
+          float4* bufN = reinterpret_cast<float4*>(sm + C::oBuf3);   // BUF3: the next step's bufH
           cta_sync();
           PROF_MARK(7);
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) {
-            bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
-            if (NH >= 2) bufH[C::row(j0) + jj * C::PSTR + pg] = z[jj];
+          for (int jj = 0; jj < kJT; ++jj) bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
+          if (NH >= 2) {
+            if constexpr (C::BUF3) {
+              const float s2 = sSl[NH - 2];
+              with_act<ACT>(act, [&](auto act_c) {
+                constexpr int AS = decltype(act_c)::value;
+#pragma unroll
+                for (int jj = 0; jj < kJT; ++jj)
+                  bufH[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+              });
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < kJT; ++jj) bufH[C::row(j0) + jj * C::PSTR + pg] = z[jj];
+            }
           }
           cta_sync();
 #pragma unroll 1
@@ -986,7 +997,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             PROF_MARK(16);
             gemm_bwd<N, NH, DO, T>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
             PROF_MARK(17);
-            st.load(k - 2, reinterpret_cast<float*>(z));
+            if constexpr (!C::BUF3) st.load(k - 2, reinterpret_cast<float*>(z));   // BUF3: z holds it already
             const float s = sSl[k - 2];
             with_act<ACT>(act, [&](auto act_c) {
               constexpr int AS = decltype(act_c)::value;
@@ -999,11 +1010,19 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
               const float s2 = sSl[k - 3];
               with_act<ACT>(act, [&](auto act_c) {
                 constexpr int AS = decltype(act_c)::value;
+                if constexpr (C::BUF3) {
+                  // H^{k-2} straight into the free buffer (nobody reads it this step);
+                  // z keeps layer k-2's raw jets for the next step's act_bwd
 #pragma unroll
-                for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+                  for (int jj = 0; jj < kJT; ++jj)
+                    bufN[C::row(j0) + jj * C::PSTR + pg] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+                } else {
+#pragma unroll
+                  for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s2, m1, m2, act);
+                }
               });
             }
-            db_sum<N, NH, DO, T, DSM>(bufZ, sDw);
+            db_sum<N, NH, DO, T, DSM>(bufZ, sDw, A + LY::offB(k));
             PROF_MARK(18);
             cta_sync();
             PROF_MARK(19);
@@ -1011,7 +1030,12 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
 #pragma unroll
             for (int jj = 0; jj < kJT; ++jj) {
               bufZ[C::row(j0) + jj * C::PSTR + pg] = hb[jj];
-              if (more) bufH[C::row(j0) + jj * C::PSTR + pg] = z[jj];
+              if (!C::BUF3 && more) bufH[C::row(j0) + jj * C::PSTR + pg] = z[jj];
+            }
+            if constexpr (C::BUF3) {
+              float4* t = bufH;
+              bufH = bufN;
+              bufN = t;
             }
             cta_sync();
           }
