@@ -24,7 +24,7 @@ namespace pinn {
 #define PINN_DWPRE_MAX 32
 #endif
 #ifndef PINN_UF_FWD
-#define PINN_UF_FWD 10
+#define PINN_UF_FWD 0   // 0 = fully unrolled (gemm_fwd)
 #endif
 #ifndef PINN_UF_BWD
 #define PINN_UF_BWD 1
@@ -160,6 +160,15 @@ __device__ __forceinline__ void fma4(float4& acc, float w, const float4& h) {
   acc = make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+// compile-time loop: f(I) for I = B, B + S, ... < E, expanded in place
+template <int B, int E, int S, class F>
+__device__ __forceinline__ void static_for(F& f) {
+  if constexpr (B < E) {
+    f(B);
+    static_for<B + S, E, S>(f);
+  }
+}
+
 // forward GEMM of one hidden layer for this thread's (point, neuron block):
 // z[jj].c = sum_i W[j][i] Hin[i][p].c  (+ b on the value channel).
 // Per i-quad all kJT jet accumulators are updated once per input component, so
@@ -172,8 +181,7 @@ __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const f
 #pragma unroll
   for (int jj = 0; jj < kJT; ++jj) z[jj] = make_float4(b[j0 + jj], 0.0f, 0.0f, 0.0f);
   const float* Wb = W + j0 * C::WS + nb * 4;
-#pragma unroll UF
-  for (int i = 0; i < N; i += 4) {
+  auto quad = [&](int i) {
     float4 h[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) h[m] = Hin[C::row(i + m) + pg];
@@ -185,6 +193,17 @@ __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const f
 #pragma unroll
       for (int jj = 0; jj < kJT; ++jj) fma4(z[jj], comp(w[jj], m), h[m]);
     }
+  };
+  if constexpr (UF == 0) {
+    // fully unrolled: the compiler unrolls width 80's 20 i-quads only 4-fold
+    // whatever the pragma says, and that loop rotates the accumulator
+    // registers across its back edge (46 MOVs per 320 FFMA2): C4 K1 15.44 ->
+    // 15.05 ms.  The per-region-activation instance (C5) keeps the loop (the
+    // larger body measured 0.3 % slower there).
+    static_for<0, N, 4>(quad);
+  } else {
+#pragma unroll UF
+    for (int i = 0; i < N; i += 4) quad(i);
   }
 }
 
@@ -839,7 +858,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           const float4* Hin = (k & 1) ? buf1 : buf0;
           float4* Hout = (k & 1) ? buf0 : buf1;
           PROF_MARK(MS == 1 ? 10 : 12);
-          gemm_fwd<N, NH, DO, T, kUfFwd>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
+          gemm_fwd<N, NH, DO, T, (ACT == kActMixed && kUfFwd == 0) ? 10 : kUfFwd>(Hin, sWh + (k - 2) * C::WROWS, sBh + (k - 2) * N, z, pg, nb);
           PROF_MARK(MS == 1 ? 10 : 13);
           const float s = sSl[k - 1];
           with_act<ACT>(act, [&](auto act_c) {
