@@ -54,6 +54,11 @@ constexpr int kUfFwd = PINN_UF_FWD, kUfDw = PINN_UF_DW;
   } while (0)
 #endif
 constexpr int kUfBwd = PINN_UF_BWD;
+// the input-adjoint GEMM's block loop fully unrolled (0) for the uniform-
+// activation width-80 instances only: C4 K1 15.06 -> 14.82 ms, while C5's
+// per-region-activation instance (+4 %) and width 40 (+3.8 %) lose with it
+template <int N, int ACT>
+constexpr int kUfBwdOf = (N == 80 && ACT != kActMixed && kUfBwd == 1) ? 0 : kUfBwd;
 
 // CTA barrier preceded by an explicit warp reconvergence.
 __device__ __forceinline__ void cta_sync() {
@@ -208,15 +213,14 @@ __device__ __forceinline__ void gemm_fwd(const float4* __restrict__ Hin, const f
 }
 
 // reverse GEMM (input adjoint): hb[ii].c = sum_j Zb[j][p].c W[j][j0 + ii]
-template <int N, int NH, int DO, int T>
+template <int N, int NH, int DO, int T, int UF>
 __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const float* __restrict__ W, float4* hb,
                                          int pg, int nb) {
   using C = KCfg<N, NH, DO, T>;
   const int j0 = nb * kJT;
 #pragma unroll
   for (int e = 0; e < kJT; ++e) hb[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-#pragma unroll kUfBwd
-  for (int jb = 0; jb < C::NB; ++jb) {
+  auto blk = [&](int jb) {
     // rows jb*kJT .. +kJT-1 share the block skew jb*4
     const float* Wrow = W + jb * (kJT * C::WS + 4) + j0;
     const float4* Zrow = Zb + C::row(jb * kJT) + pg;   // rows of one block share its skew
@@ -231,6 +235,12 @@ __device__ __forceinline__ void gemm_bwd(const float4* __restrict__ Zb, const fl
         fma4(hb[2 * q + 1], w.y, zb);
       }
     }
+  };
+  if constexpr (UF == 0) {
+    static_for<0, C::NB, 1>(blk);
+  } else {
+#pragma unroll UF
+    for (int jb = 0; jb < C::NB; ++jb) blk(jb);
   }
 }
 
@@ -258,8 +268,7 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
 #pragma unroll
       for (int ii = 0; ii < IB; ++ii) acc2[jj][ii] = make_float2(0.0f, 0.0f);
     }
-#pragma unroll UF
-    for (int p = s * PS; p < (s + 1) * PS; ++p) {
+    auto pt = [&](int p) {
       float4 zr[JB], hr[IB];
 #pragma unroll
       for (int jj = 0; jj < JB; ++jj) zr[jj] = Zb[C::row(jb + NJ * jj) + p];
@@ -272,6 +281,13 @@ __device__ __forceinline__ void gemm_dw(const float4* __restrict__ Zb, const flo
           acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].x, zr[jj].y), make_float2(hr[ii].x, hr[ii].y), acc2[jj][ii]);
           acc2[jj][ii] = __ffma2_rn(make_float2(zr[jj].z, zr[jj].w), make_float2(hr[ii].z, hr[ii].w), acc2[jj][ii]);
         }
+    };
+    if constexpr (UF == 0) {
+      auto ptS = [&](int p) { pt(s * PS + p); };
+      static_for<0, PS, 1>(ptS);
+    } else {
+#pragma unroll UF
+      for (int p = s * PS; p < (s + 1) * PS; ++p) pt(p);
     }
     float acc[JB][IB];
 #pragma unroll
@@ -1014,7 +1030,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             gemm_dw_prefetch<N, NH, DO, T, DSM>(A + LY::offW(k), A + LY::offB(k), first, pre, preb);
             // adjoint of H^{k-1}, then of Z^{k-1}
             PROF_MARK(16);
-            gemm_bwd<N, NH, DO, T>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
+            gemm_bwd<N, NH, DO, T, kUfBwdOf<N, ACT>>(bufZ, sWh + (k - 2) * C::WROWS, hb, pg, nb);
             PROF_MARK(17);
             if constexpr (!C::BUF3) st.load(k - 2, reinterpret_cast<float*>(z));   // BUF3: z holds it already
             const float s = sSl[k - 2];
