@@ -336,12 +336,23 @@ int chunk_tiles(int cnt, int P, int acc, bool interior = true) {
   }();
   const int tiles = (cnt + P - 1) / P;
   const int m = std::min(4, std::max(1, acc / 2048));
+  // a small-partial net (m = 1: width 20) with runs of at most two waves of
+  // the 296 CTA slots of its 128-thread instance takes one-tile chunks
+  // (interface runs included): the C3 weak-scaling subdomain (20k points, 315
+  // tiles) then spreads over every slot instead of 105 three-tile chunks
+  // (step 77.0 -> 69.5 us; C3 x 8 per GPU 0.272 -> 0.274 ms, its K5 reads 3x
+  // the partials; with 2-tile interface chunks it was 0.293 ms)
+  if (!min_env && m == 1 && tiles <= 2 * 296) return 1;
   const int min_tiles = min_env ? min_env : (tiles >= 200 ? m : 2);
   (void)interior;
   // a giant run (the data-parallel comparator's single subdomain: 7,530 tiles
   // of 32) would get only ~128 chunks -- fewer than the persistent CTAs -- so
   // runs of > 2048 tiles with partials of <= 64 KB may use up to 1024 chunks
-  const int max_chunks = (tiles > 2048 && acc <= 16384) ? 1024 : 148;
+  static const int maxc_env = [] {   // development knob: PINN_DD_MAX_CHUNKS
+    const char* e = std::getenv("PINN_DD_MAX_CHUNKS");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int max_chunks = maxc_env ? maxc_env : ((tiles > 2048 && acc <= 16384) ? 1024 : 148);
   return std::max(min_tiles, (tiles + max_chunks - 1) / max_chunks);
 }
 
