@@ -929,8 +929,14 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           const int p = idx % C::P, o = idx / C::P;
           float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
           const float* w = sWo + o * C::WS;
-#pragma unroll 4
-          for (int i = qq; i < N; i += 4) fma4(acc, w[i], HL[C::row(i) + p]);
+          // constant trip count (N / 4 for every qq): fully unrolled, so all
+          // its shared loads issue up front (the 4-fold unrolled loop stalled
+          // on the shared-load scoreboard)
+#pragma unroll
+          for (int ii = 0; ii < N / 4; ++ii) {
+            const int i = qq + 4 * ii;
+            fma4(acc, w[i], HL[C::row(i) + p]);
+          }
 #pragma unroll
           for (int off = 1; off < 4; off <<= 1) {
             acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
@@ -977,8 +983,9 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             // global chunk partial: its current value is loaded before the dot product
             const float prev = (!DSM && qq == 0 && !first) ? __ldcg(A + LY::offW(NH + 1) + idx) : 0.0f;
             float2 a2 = make_float2(0.0f, 0.0f);   // channel pairs (x.x + z.z, y.y + w.w)
-#pragma unroll 4
-            for (int p = qq; p < C::P; p += 4) {
+#pragma unroll
+            for (int pp = 0; pp < C::P / 4; ++pp) {
+              const int p = qq + 4 * pp;
               const float4 h = HL[C::row(i) + p];
               const float4 ub = sU[p * DO + o];
               a2 = __ffma2_rn(make_float2(h.x, h.y), make_float2(ub.x, ub.y), a2);
@@ -1114,8 +1121,9 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             const float p1 = pf ? __ldcg(A + LY::offW(1) + 2 * j + 1) : 0.0f;
             const float pb = pf ? __ldcg(A + LY::offB(1) + j) : 0.0f;
             float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
-#pragma unroll 4
-            for (int p = qq; p < C::P; p += 4) {
+#pragma unroll
+            for (int pp = 0; pp < C::P / 4; ++pp) {
+              const int p = qq + 4 * pp;
               const float4 zb = bufZ[C::row(j) + p];
               a0 = fmaf(zb.x, sX[p], a0) + zb.y;
               a1 = fmaf(zb.x, sY[p], a1) + zb.z;
