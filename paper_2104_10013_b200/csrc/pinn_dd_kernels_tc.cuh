@@ -62,10 +62,13 @@ __device__ __forceinline__ int sw32(int r, int c) {
   return (((r >> 2) * NA + (c >> 5)) * 512 + (b ^ (((b >> 7) & 3) << 5))) >> 2;
 }
 
+// round to the nearest tf32, ties away from zero: the value cvt.rna.tf32.f32
+// gives for every finite x (half a tf32 ulp added to the sign-magnitude bits,
+// a mantissa carry moves into the exponent), in two integer instructions --
+// sm_100 has no native cvt.rna.tf32, its emulation took four (FSETP, SEL, LOP3,
+// IADD3) per operand value.  Non-finite inputs stay non-finite.
 __device__ __forceinline__ float to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 // shared-memory matrix descriptor (layout type 1 = SWIZZLE_128B_BASE32B)
