@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
             const int qq = t4 & 3, idx = t4 >> 2;
             const int o = idx / N, i = idx % N;
             // global chunk partial: its current value is loaded before the dot product
-            const float prev = (!DSM && qq == 0 && !first) ? __ldcg(A + LY::offW(NH + 1) + idx) : 0.0f;
+            [[maybe_unused]] const float prev = (!DSM && qq == 0 && !first) ? __ldcg(A + LY::offW(NH + 1) + idx) : 0.0f;
             float2 a2 = make_float2(0.0f, 0.0f);   // channel pairs (x.x + z.z, y.y + w.w)
 #pragma unroll
             for (int pp = 0; pp < C::P / 4; ++pp) {
@@ -1117,9 +1117,9 @@ __global__ void __launch_bounds__(T, 256 / T) k_fused(const KArgs a) {
           for (int t4 = tid; t4 < 4 * N; t4 += T) {
             const int qq = t4 & 3, j = t4 >> 2;
             const bool pf = !DSM && qq == 0 && !first;   // global partial: load before the sums
-            const float p0 = pf ? __ldcg(A + LY::offW(1) + 2 * j) : 0.0f;
-            const float p1 = pf ? __ldcg(A + LY::offW(1) + 2 * j + 1) : 0.0f;
-            const float pb = pf ? __ldcg(A + LY::offB(1) + j) : 0.0f;
+            [[maybe_unused]] const float p0 = pf ? __ldcg(A + LY::offW(1) + 2 * j) : 0.0f;
+            [[maybe_unused]] const float p1 = pf ? __ldcg(A + LY::offW(1) + 2 * j + 1) : 0.0f;
+            [[maybe_unused]] const float pb = pf ? __ldcg(A + LY::offB(1) + j) : 0.0f;
             float a0 = 0.0f, a1 = 0.0f, ab = 0.0f;
 #pragma unroll
             for (int pp = 0; pp < C::P / 4; ++pp) {
