@@ -447,8 +447,12 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
       if (tid < 4) a.partial_loss[size_t(c) * 4 + tid] = 0.0f;
     }
 
-    auto chunk_body = [&](auto act_c, auto mode_c) {
-      constexpr int AS = decltype(act_c)::value;
+    // the chunk body is compiled once per mode; a per-subdomain-activation
+    // instance branches on `act` around each activation loop only (with_act),
+    // never around the MMAs, operand stores or epilogue (compiling the whole
+    // body per activation tripled C5's kernel to 21 k instructions and made
+    // instruction fetch its top stall)
+    auto chunk_body = [&](auto mode_c) {
       constexpr int MS = decltype(mode_c)::value;   // 0 loss + gradient, 1 payload
       float lsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       // coordinates of the next tile are loaded into registers while the
@@ -486,11 +490,15 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             const int j = w.j(jj);
             const float w0 = sW1[2 * j], w1 = sW1[2 * j + 1];
             z[jj] = make_float4(fmaf(w0, x, fmaf(w1, y, sB1[j])), w0, w1, 0.0f);
-            z[jj].x = stash_x<AS>(z[jj].x, s, act);
           }
-          if constexpr (MS == 0) tstore(tm, w, 80 * 1, z);
+          with_act<ACT>(act, [&](auto act_c) {
+            constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
+            for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
+            if constexpr (MS == 0) tstore(tm, w, 80 * 1, z);
+#pragma unroll
+            for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
+          });
           owrite(sH, w, z);
         }
 #pragma unroll 1
@@ -526,11 +534,14 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           PROF_MARK(MS == 1 ? 10 : 13);
           tload(tm, w, 0, z);
           const float s = sSl[k - 1];
+          with_act<ACT>(act, [&](auto act_c) {
+            constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
-          if constexpr (MS == 0) tstore(tm, w, 80 * k, z);   // stash form (t for tanh)
+            for (int jj = 0; jj < kJT; ++jj) z[jj].x = stash_x<AS>(z[jj].x, s, act);
+            if constexpr (MS == 0) tstore(tm, w, 80 * k, z);   // stash form (t for tanh)
 #pragma unroll
-          for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
+            for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
+          });
           if (k < NH) owrite(sH, w, z);   // the MMA that read H^{k-1} has completed
         }
         PROF_MARK(MS == 1 ? 10 : 4);
@@ -646,14 +657,20 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
             tload(tm, w, 80 * k, z);
             {
               const float s = sSl[k - 1];
+              with_act<ACT>(act, [&](auto act_c) {
+                constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-              for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+                for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+              });
             }
             tload(tm, w, 80 * (k - 1), z);
             {
               const float s = sSl[k - 2];
+              with_act<ACT>(act, [&](auto act_c) {
+                constexpr int AS = decltype(act_c)::value;
 #pragma unroll
-              for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
+                for (int jj = 0; jj < kJT; ++jj) z[jj] = act_fwd<AS>(z[jj], s, m1, m2, act);
+              });
             }
             PROF_MARK(16);
             wait_dw();   // the previous dW MMA has read Zb / H: they may be overwritten
@@ -694,9 +711,14 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
           {
             const float s = sSl[0];
             const float x = sX[w.pt], y = sY[w.pt];
+            with_act<ACT>(act, [&](auto act_c) {
+              constexpr int AS = decltype(act_c)::value;
+#pragma unroll
+              for (int jj = 0; jj < kJT; ++jj) hb[jj] = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+            });
 #pragma unroll
             for (int jj = 0; jj < kJT; ++jj) {
-              const float4 zb = act_bwd<AS>(z[jj], hb[jj], s, m1, m2, act);
+              const float4 zb = hb[jj];
               float v0 = fmaf(zb.x, x, zb.y), v1 = fmaf(zb.x, y, zb.z), vb = zb.x;
 #pragma unroll
               for (int off = 4; off < 32; off <<= 1) {
@@ -737,25 +759,13 @@ __global__ void __launch_bounds__(tc::T, 1) k_fused_tc(const KArgs a) {
         }
       }
     };
-    auto by_mode = [&](auto act_c) {
-      if constexpr (MODE == 2) {
-        if (pay)
-          chunk_body(act_c, std::integral_constant<int, 1>{});
-        else
-          chunk_body(act_c, std::integral_constant<int, 0>{});
-      } else {
-        chunk_body(act_c, std::integral_constant<int, MODE>{});
-      }
-    };
-    if constexpr (ACT == kActMixed) {
-      if (act == 0)
-        by_mode(std::integral_constant<int, 0>{});
-      else if (act == 1)
-        by_mode(std::integral_constant<int, 1>{});
+    if constexpr (MODE == 2) {
+      if (pay)
+        chunk_body(std::integral_constant<int, 1>{});
       else
-        by_mode(std::integral_constant<int, 2>{});
+        chunk_body(std::integral_constant<int, 0>{});
     } else {
-      by_mode(std::integral_constant<int, ACT>{});
+      chunk_body(std::integral_constant<int, MODE>{});
     }
     if (MODE == 2 && pay) {
       cta_sync();
