@@ -698,11 +698,19 @@ pinn_dd_status launch_k1(pinn_dd* h, int part = 0) {
 }
 // mode 0: reduce + slopes (loss_grad); 1: reduce + slopes + Adam (step);
 // 2: Adam on the stored gradient (pinn_dd_adam)
+// K5a with 512-thread blocks for nets of at most this many partial floats
+// (width 20: C3's weak-scaling subdomain, 315 one-tile chunk partials over 14
+// entry blocks)
+constexpr int kSmallNet = 4096;
 pinn_dd_status launch_k5(pinn_dd* h, int mode) {
   dim3 g((h->pstride + kRB - 1) / kRB, h->d.n_sub);
   if (mode != 2) {
     // status bits of this evaluation start at 0 (zeroed at create and by the K5b that published the last ones)
-    k_reduce<<<dim3((h->pstride + kRW - 1) / kRW, h->d.n_sub), kRB, 0, h->stream>>>(make_rargs(h, 0));
+    const dim3 g5a((h->pstride + kRW - 1) / kRW, h->d.n_sub);
+    if (h->pstride <= kSmallNet)
+      k_reduce<512><<<g5a, 512, 0, h->stream>>>(make_rargs(h, 0));
+    else
+      k_reduce<kRB><<<g5a, kRB, 0, h->stream>>>(make_rargs(h, 0));
     ++h->launches;
     CK(h, cudaGetLastError());
   }

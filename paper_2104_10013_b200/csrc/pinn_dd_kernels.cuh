@@ -1273,9 +1273,13 @@ struct RArgs {
 // instead of 8 (C3's single subdomain: 105 chunk partials of 7 blocks were a
 // 20 us latency chain).  Indices that are not parameters (16-B padding, slope
 // slots) are never written by K1; the partial region is zeroed once at create.
+// RB threads per block: 256, or 512 for small nets (width 20: few entry
+// blocks, so 16 warps per block halve each warp's chain of chunk rows; the
+// choice depends only on the net, so it is the same under every placement)
 constexpr int kRW = 128;   // entries per K5a block
-__global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
-  __shared__ double red[kRB / 32][kRW];
+template <int RB>
+__global__ void __launch_bounds__(RB) k_reduce(const RArgs r) {
+  __shared__ double red[RB / 32][kRW];
   const int q = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int i0 = blockIdx.x * kRW;
@@ -1285,7 +1289,7 @@ __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
   {
     double g[4] = {0.0, 0.0, 0.0, 0.0};
     if (i < r.pstride) {
-      constexpr int NW = kRB / 32;
+      constexpr int NW = RB / 32;
       const float4* src = reinterpret_cast<const float4*>(r.partial + i);
       const size_t cs = size_t(r.pstride) / 4;   // float4 per partial
       int c = c0 + w;
@@ -1310,7 +1314,7 @@ __global__ void __launch_bounds__(kRB) k_reduce(const RArgs r) {
   if (w == 0) {
     double g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int ww = 0; ww < kRB / 32; ++ww)
+    for (int ww = 0; ww < RB / 32; ++ww)
 #pragma unroll
       for (int e = 0; e < 4; ++e) g[e] += red[ww][4 * lane + e];
     if (i < r.pstride) {
